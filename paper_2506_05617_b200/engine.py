@@ -1,0 +1,365 @@
+"""Device orchestration of the LFA hot path over the C-ABI.
+
+PyTorch is used only as plumbing here: device memory (caching allocator),
+the current CUDA stream, events and torch.distributed.  Every byte of
+compute is one of the library's sm_100a kernels, reached through _lib:
+
+    K1  cs_symbol_field        half-grid symbol assembly
+    K2/3 cs_batched_svd(_grouped)  one-sided Jacobi + per-block epilogue
+    cs_complete_zero_columns / cs_first_failure / cs_spectrum_values
+
+All tensors stay on the device; host copies happen only where the drop-in
+API returns numpy arrays.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import AllocationFailure, ConvergenceFailure
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+DEFAULT_MAX_SWEEPS = 100   # blocksvd.py:25
+DEFAULT_SVD_TOL = 1e-13    # blocksvd.py:26
+
+
+def require_cuda(device=None):
+    """Resolve the target device; fail loudly without CUDA (no CPU fallback)."""
+    if torch is None or not torch.cuda.is_available():
+        raise RuntimeError("convspectra_b200 needs a CUDA device (B200); no CPU fallback exists")
+    _lib.load()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise RuntimeError(f"convspectra_b200 computes on CUDA devices only, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def dtype_code(dtype: str) -> int:
+    if dtype == "f32":
+        return _lib.CS_F32
+    if dtype == "f64":
+        return _lib.CS_F64
+    raise ValueError(f"unknown dtype {dtype!r} (expected 'f32' or 'f64')")
+
+
+def real_dtype(dtype: str):
+    return torch.float32 if dtype == "f32" else torch.float64
+
+
+def complex_dtype(dtype: str):
+    return torch.complex64 if dtype == "f32" else torch.complex128
+
+
+def dtype_of_tensor(t) -> str:
+    if t.dtype in (torch.complex64, torch.float32):
+        return "f32"
+    return "f64"
+
+
+def effective_tol(tol: float, dtype: str, rows: int) -> float:
+    """Convergence threshold actually used by the kernel.
+
+    fp64 uses the caller's tol (reference default 1e-13, blocksvd.py:26).
+    fp32 cannot resolve |gamma|/sqrt(alpha*beta) below its rounding floor
+    (~eps32*sqrt(rows)); the threshold is floored at 1e-6*sqrt(rows/64) so the
+    sweep loop terminates (measured: 12-13 sweeps at 256x256, sigma within
+    2e-7 of the fp64 reference, oracle/oracle.c *_f32acc study)."""
+    if dtype == "f64":
+        return float(tol)
+    return max(float(tol), 1e-6 * math.sqrt(max(rows, 1) / 64.0))
+
+
+def stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class _Workspace:
+    """Grow-only device scratch per device (the C-ABI owns no memory)."""
+
+    def __init__(self):
+        self._buf = {}
+
+    def get(self, device, nbytes: int):
+        if nbytes <= 0:
+            return None
+        key = (device.type, device.index)
+        buf = self._buf.get(key)
+        if buf is None or buf.numel() < nbytes:
+            self._buf[key] = None
+            buf = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+            self._buf[key] = buf
+        return buf
+
+
+WORKSPACE = _Workspace()
+
+
+def half_grid_count(n: int, m: int) -> int:
+    """Conjugate-orbit representatives, same as cs_half_grid_count."""
+    h0 = m // 2 + 1
+    nmid = (n - 1) // 2
+    return h0 + nmid * m + (h0 if (n % 2 == 0 and n > 1) else 0)
+
+
+def half_grid_indices(n: int, m: int) -> np.ndarray:
+    """Full-grid index f of each representative, in representative order."""
+    h0 = m // 2 + 1
+    rows = [np.arange(h0)]
+    for i in range(1, (n - 1) // 2 + 1):
+        rows.append(i * m + np.arange(m))
+    if n % 2 == 0 and n > 1:
+        rows.append((n // 2) * m + np.arange(h0))
+    return np.concatenate(rows).astype(np.int64)
+
+
+def partner_map(n: int, m: int):
+    """For each full-grid f: (representative index u, conj flag)."""
+    f = np.arange(n * m)
+    i, j = f // m, f % m
+    fs = ((n - i) % n) * m + (m - j) % m
+    rep = f <= fs
+    frep = np.where(rep, f, fs)
+    reps = half_grid_indices(n, m)
+    lut = np.full(n * m, -1, dtype=np.int64)
+    lut[reps] = np.arange(len(reps))
+    return lut[frep], ~rep
+
+
+def self_conjugate_count(n: int, m: int) -> int:
+    return (1 + (n % 2 == 0)) * (1 + (m % 2 == 0))
+
+
+# ---------------------------------------------------------------------------
+# K1
+# ---------------------------------------------------------------------------
+def weights_to_device(kernel, dtype: str, device):
+    w = kernel.device_weights(dtype)
+    return torch.from_numpy(w).to(device, non_blocking=False)
+
+
+def symbol_field(w_dev, dims_n: int, dims_m: int, dtype: str, half: bool = True,
+                 f_first: int = 0, f_count: int | None = None, out=None, layout: int = 0):
+    """Symbol blocks for a contiguous range of (representative or full-grid) frequencies."""
+    co, ci, kh, kw = w_dev.shape
+    total = half_grid_count(dims_n, dims_m) if half else dims_n * dims_m
+    if f_count is None:
+        f_count = total - f_first
+    if out is None:
+        shape = (f_count, co, ci) if layout == 0 else (co, ci, f_count)
+        out = torch.empty(shape, dtype=complex_dtype(dtype), device=w_dev.device)
+    st = _lib.load().cs_symbol_field(ptr(w_dev), dtype_code(dtype), co, ci, kh, kw, dims_n,
+                                     dims_m, f_first, f_count, int(half), ptr(out), layout,
+                                     stream_ptr(w_dev.device))
+    _lib.check(st, "cs_symbol_field")
+    return out
+
+
+def symbol_at_freqs(w_dev, freqs: np.ndarray, dtype: str):
+    co, ci, kh, kw = w_dev.shape
+    fr = torch.from_numpy(np.ascontiguousarray(freqs, dtype=np.float64)).to(w_dev.device)
+    out = torch.empty((len(freqs), co, ci), dtype=complex_dtype(dtype), device=w_dev.device)
+    st = _lib.load().cs_symbol_at(ptr(w_dev), dtype_code(dtype), co, ci, kh, kw, ptr(fr),
+                                  len(freqs), ptr(out), stream_ptr(w_dev.device))
+    _lib.check(st, "cs_symbol_at")
+    return out
+
+
+def expand_half(half, n: int, m: int, dtype: str, out=None):
+    F_u, a, b = half.shape
+    if out is None:
+        out = torch.empty((n * m, a, b), dtype=half.dtype, device=half.device)
+    st = _lib.load().cs_expand_half_grid(ptr(half), dtype_code(dtype), a, b, n, m, ptr(out),
+                                         stream_ptr(half.device))
+    _lib.check(st, "cs_expand_half_grid")
+    return out
+
+
+def is_conj_symmetric(full, n: int, m: int, dtype: str) -> bool:
+    F, a, b = full.shape
+    flag = torch.empty(1, dtype=torch.int32, device=full.device)
+    st = _lib.load().cs_check_conj_symmetry(ptr(full), dtype_code(dtype), a, b, n, m, ptr(flag),
+                                            stream_ptr(full.device))
+    _lib.check(st, "cs_check_conj_symmetry")
+    return bool(flag.item())
+
+
+# ---------------------------------------------------------------------------
+# K2/K3
+# ---------------------------------------------------------------------------
+@dataclass
+class SvdBatch:
+    sigma: "torch.Tensor"          # (count, r) descending, real
+    info: "torch.Tensor"           # (count,) int32 sweeps or -1
+    U: "torch.Tensor | None" = None  # (count, c_out, r)
+    V: "torch.Tensor | None" = None  # (count, c_in, r)
+    zero: "torch.Tensor | None" = None
+
+
+def alloc_svd_outputs(count, co, ci, dtype, want_vectors, device):
+    r = min(co, ci)
+    sig = torch.empty((count, r), dtype=real_dtype(dtype), device=device)
+    info = torch.empty((count,), dtype=torch.int32, device=device)
+    U = V = zero = None
+    if want_vectors:
+        U = torch.empty((count, co, r), dtype=complex_dtype(dtype), device=device)
+        V = torch.empty((count, ci, r), dtype=complex_dtype(dtype), device=device)
+        zero = torch.empty((count,), dtype=torch.int32, device=device)
+    return SvdBatch(sig, info, U, V, zero)
+
+
+def batched_svd(blocks, dtype: str, want_vectors: bool, tol=DEFAULT_SVD_TOL,
+                max_sweeps=DEFAULT_MAX_SWEEPS, out: SvdBatch | None = None,
+                complete=True) -> SvdBatch:
+    """SVD of every (c_out, c_in) block of a contiguous device tensor."""
+    count, co, ci = blocks.shape
+    dev = blocks.device
+    lib = _lib.load()
+    if out is None:
+        out = alloc_svd_outputs(count, co, ci, dtype, want_vectors, dev)
+    code = dtype_code(dtype)
+    ws_bytes = lib.cs_batched_svd_workspace(code, count, co, ci, int(want_vectors))
+    ws = WORKSPACE.get(dev, ws_bytes)
+    etol = effective_tol(tol, dtype, max(co, ci))
+    st = lib.cs_batched_svd(ptr(blocks), code, count, co, ci, int(want_vectors), etol,
+                            int(max_sweeps), ptr(out.sigma), ptr(out.U), ptr(out.V),
+                            ptr(out.info), ptr(out.zero), ptr(ws), ws_bytes, stream_ptr(dev))
+    _lib.check(st, "cs_batched_svd")
+    if want_vectors and complete:
+        complete_zero_columns(out, co, ci, dtype)
+    return out
+
+
+def batched_svd_grouped(groups, dtype: str, want_vectors: bool, tol=DEFAULT_SVD_TOL,
+                        max_sweeps=DEFAULT_MAX_SWEEPS):
+    """One call over heterogeneous layers: groups = [blocks tensor, ...]."""
+    lib = _lib.load()
+    outs = []
+    table = (_lib.SvdGroup * len(groups))()
+    dev = groups[0].device
+    rows = 1
+    for g, blk in enumerate(groups):
+        count, co, ci = blk.shape
+        o = alloc_svd_outputs(count, co, ci, dtype, want_vectors, dev)
+        outs.append(o)
+        table[g] = _lib.SvdGroup(ptr(blk), count, co, ci, ptr(o.sigma), ptr(o.U), ptr(o.V),
+                                 ptr(o.info), ptr(o.zero))
+        rows = max(rows, co, ci)
+    code = dtype_code(dtype)
+    ws_bytes = lib.cs_batched_svd_grouped_workspace(table, len(groups), code, int(want_vectors))
+    ws = WORKSPACE.get(dev, ws_bytes)
+    # one tol for the call: floor of the largest block (conservative for fp32)
+    etol = effective_tol(tol, dtype, rows)
+    st = lib.cs_batched_svd_grouped(table, len(groups), code, int(want_vectors), etol,
+                                    int(max_sweeps), ptr(ws), ws_bytes, stream_ptr(dev))
+    _lib.check(st, "cs_batched_svd_grouped")
+    if want_vectors:
+        for blk, o in zip(groups, outs):
+            complete_zero_columns(o, blk.shape[1], blk.shape[2], dtype)
+    return outs
+
+
+def complete_zero_columns(out: SvdBatch, co: int, ci: int, dtype: str):
+    """blocksvd.py:184-198 on the factor of the working (tall) matrix."""
+    if out.zero is None or out.sigma.shape[0] == 0:
+        return
+    wide = co < ci
+    Uw = out.V if wide else out.U
+    mr = ci if wide else co
+    r = min(co, ci)
+    st = _lib.load().cs_complete_zero_columns(ptr(Uw), dtype_code(dtype), out.sigma.shape[0], mr,
+                                              r, ptr(out.sigma), ptr(out.zero),
+                                              stream_ptr(out.sigma.device))
+    _lib.check(st, "cs_complete_zero_columns")
+
+
+def first_failure(info) -> int:
+    first = torch.empty(1, dtype=torch.int64, device=info.device)
+    st = _lib.load().cs_first_failure(ptr(info), info.shape[0], ptr(first),
+                                      stream_ptr(info.device))
+    _lib.check(st, "cs_first_failure")
+    return int(first.item())
+
+
+def spectrum_values(sigma, dtype: str, n: int, m: int, half: bool):
+    """Flat descending float64 values on the device (conj partners duplicated)."""
+    count, r = sigma.shape
+    nv = n * m * r if half else count * r
+    lib = _lib.load()
+    code = dtype_code(dtype)
+    ws_bytes = lib.cs_spectrum_values_workspace(nv, code)
+    ws = WORKSPACE.get(sigma.device, ws_bytes)
+    values = torch.empty((nv,), dtype=torch.float64, device=sigma.device)
+    st = lib.cs_spectrum_values(ptr(sigma), code, count, r, n, m, int(half), ptr(values), ptr(ws),
+                                ws_bytes, stream_ptr(sigma.device))
+    _lib.check(st, "cs_spectrum_values")
+    return values
+
+
+def raise_convergence(f: int, freqs=None, max_sweeps=DEFAULT_MAX_SWEEPS):
+    """Reference message shape of blocksvd.py:213-224."""
+    where = f"block {f}"
+    if freqs is not None:
+        k = freqs[f]
+        where = f"frequency index {f} (k=({k[0]:.6g}, {k[1]:.6g}))"
+    raise ConvergenceFailure(
+        f"jacobi SVD did not converge within {max_sweeps} sweeps at {where}; "
+        "check the input for NaN/Inf contamination")
+
+
+def device_budget_bytes(device, mem_budget_gib=None) -> int:
+    """Field budget for device-resident paths: the explicit parameter, then the
+    reference's env knob, else the device's total memory."""
+    if mem_budget_gib is not None:
+        return int(float(mem_budget_gib) * 2**30)
+    env = os.environ.get("CONV_SPECTRA_MEM_BUDGET_GIB")
+    if env is not None:
+        return int(float(env) * 2**30)
+    return int(torch.cuda.get_device_properties(device).total_memory)
+
+
+def check_budget(need: int, budget: int, what: str):
+    if need > budget:
+        raise AllocationFailure(f"{what} needs {need} bytes, budget is {budget} bytes")
+
+
+class Timer:
+    """CUDA-event phase timer on the current stream of `device`."""
+
+    def __init__(self, device):
+        self.device = device
+        self.events = {}
+
+    def mark(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self.device))
+        self.events[name] = ev
+
+    def seconds(self, a, b) -> float:
+        self.events[b].synchronize()
+        return self.events[a].elapsed_time(self.events[b]) / 1e3
+
+
+def fma_peak_flops(dtype: str = "f32", device_index: int = 0) -> float:
+    """Measured FFMA/DFMA throughput (flop/s) for the roofline denominator."""
+    return float(_lib.load().cs_measure_fma_peak(dtype_code(dtype), device_index))
+
+
+_ = ctypes  # keep import for type users

@@ -1,0 +1,121 @@
+"""End-to-end spectrum computation: the drop-in ``compute_spectrum``.
+
+The reference dispatches on ``method`` at pkg/src/convspectra/pipeline.py:
+52-68; the "lfa" branch (build_symbol_field -> spectrum_from_field) is the
+hot path this package replaces.  The B200 path never materialises the full
+field: K1 assembles the conjugate-orbit representatives straight into HBM,
+the batched Jacobi solves them in place, and the spectrum assembly emits
+every value twice for non-self-conjugate representatives before one device
+sort.  With ``values_only=False`` the factors are computed and discarded,
+exactly as the reference does (pipeline.py:37-43, 69); use
+``spectrum_from_field`` or :func:`lfa_device` to keep them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import engine
+from .blocksvd import PhaseTimings, SpectrumResult, resolve_workers
+from .engine import DEFAULT_MAX_SWEEPS, DEFAULT_SVD_TOL
+from .kernels import ConvKernel, SpatialDims, validate_kernel
+from .symbol import BLOCK_CONTIGUOUS, LAYOUTS, _resolve_dtype
+
+METHODS = ("lfa", "fft", "explicit")
+PERIODIC = "periodic"
+DIRICHLET = "dirichlet"
+BOUNDARIES = (PERIODIC, DIRICHLET)
+
+
+@dataclass
+class DeviceSpectrum:
+    """Device-resident outputs of one LFA solve over representatives [u0, u0+count)."""
+
+    values: object          # float64 (n*m*r,) descending, or None when sharded
+    sigma: object           # (count, r) per representative, descending
+    U: object               # (count, c_out, r) or None
+    V: object               # (count, c_in, r) or None
+    info: object            # (count,) int32 sweeps or -1
+    u0: int
+    count: int
+    dtype: str
+
+
+def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
+               tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
+               u0: int = 0, count: int | None = None, assemble: bool = True,
+               timer: engine.Timer | None = None, field_out=None) -> DeviceSpectrum:
+    """K1 -> K2/K3 -> assembly on the current stream, no host synchronisation."""
+    total = engine.half_grid_count(n, m)
+    if count is None:
+        count = total - u0
+    if timer:
+        timer.mark("t0")
+    fld = engine.symbol_field(w_dev, n, m, dtype, half=True, f_first=u0, f_count=count,
+                              out=field_out)
+    if timer:
+        timer.mark("t1")
+    out = engine.batched_svd(fld, dtype, want_vectors, tol, max_sweeps)
+    if timer:
+        timer.mark("t2")
+    values = None
+    if assemble and u0 == 0 and count == total:
+        values = engine.spectrum_values(out.sigma, dtype, n, m, True)
+    if timer:
+        timer.mark("t3")
+    return DeviceSpectrum(values, out.sigma, out.U, out.V, out.info, u0, count, dtype)
+
+
+def field_bytes(kernel_or_shape, n: int, m: int, dtype: str, want_vectors: bool) -> int:
+    co, ci = kernel_or_shape
+    esz = 8 if dtype == "f32" else 16
+    F_u = engine.half_grid_count(n, m)
+    r = min(co, ci)
+    need = F_u * co * ci * esz
+    if want_vectors:
+        need += F_u * (co + ci) * r * esz
+    return need
+
+
+def compute_spectrum(kernel: ConvKernel, dims: SpatialDims, method: str = "lfa",
+                     boundary: str = PERIODIC, values_only: bool = True, workers: int = 0,
+                     layout: str = BLOCK_CONTIGUOUS, size_cap=None, mem_budget_gib=None,
+                     tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS, *,
+                     device=None, dtype=None,
+                     return_device_tensors: bool = False) -> SpectrumResult:
+    """Full singular value spectrum with device phase timings attached
+    (pipeline.py:24-69).  Only the LFA method is on this package's hot path;
+    "fft" and "explicit" are the reference's comparison/oracle routes."""
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    if boundary not in BOUNDARIES:
+        raise ValueError(f"unknown boundary {boundary!r}")
+    if boundary == DIRICHLET and method != "explicit":
+        raise ValueError(f"method {method!r} only supports periodic boundaries")
+    if method != "lfa":
+        raise NotImplementedError(
+            f"method {method!r} is outside the B200 hot path (only 'lfa' is implemented)")
+    if layout not in LAYOUTS:
+        raise ValueError(f"unknown layout {layout!r}")
+    resolve_workers(workers)
+    validate_kernel(kernel)
+    dev = engine.require_cuda(device)
+    dt = _resolve_dtype(kernel, dtype)
+    n, m = dims.n, dims.m
+    co, ci = kernel.c_out, kernel.c_in
+    engine.check_budget(field_bytes((co, ci), n, m, dt, not values_only),
+                        engine.device_budget_bytes(dev, mem_budget_gib),
+                        f"LFA solve ({engine.half_grid_count(n, m)} blocks of {co}x{ci})")
+    w = engine.weights_to_device(kernel, dt, dev)
+    tm = engine.Timer(dev)
+    res = lfa_device(w, n, m, dt, not values_only, tol, max_sweeps, timer=tm)
+    f = engine.first_failure(res.info)
+    if f >= 0:
+        reps = engine.half_grid_indices(n, m)
+        from .kernels import FrequencyGrid
+        engine.raise_convergence(int(reps[f]), FrequencyGrid(dims).frequencies, max_sweeps)
+    timings = PhaseTimings.build(tm.seconds("t0", "t1"), tm.seconds("t1", "t3"), 0.0)
+    values = res.values.cpu().numpy()
+    return SpectrumResult(values=values, method="lfa", boundary=PERIODIC, dims=dims,
+                          channels=(ci, co), timings=timings,
+                          device_values=res.values if return_device_tensors else None)

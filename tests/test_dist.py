@@ -1,0 +1,73 @@
+"""Frequency sharding host logic on CPU: world_size 2 over gloo.
+
+The GPU path (lfa_sharded) adds only the device solve per shard; here the
+partition and the sigma all-gather + assembly order are checked with CPU
+tensors (the collective is the same torch.distributed call NCCL runs)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2506_05617_b200 import engine
+from paper_2506_05617_b200.distributed import gather_sigma, shard_range
+
+
+@pytest.mark.parametrize("total", [1, 7, 514, 32770])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_range_partitions(total, world):
+    spans = [shard_range(total, g, world) for g in range(world)]
+    assert spans[0][0] == 0
+    for (s0, c0), (s1, _) in zip(spans, spans[1:]):
+        assert s0 + c0 == s1
+    assert sum(c for _, c in spans) == total
+    counts = [c for _, c in spans]
+    assert max(counts) - min(counts) <= 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, m, r, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    total = engine.half_grid_count(n, m)
+    u0, cnt = shard_range(total, rank, world)
+    # each rank "solves" its representatives: sigma row u = [u, u/2, ...]
+    sig = torch.stack([torch.arange(u0, u0 + cnt, dtype=torch.float64) / (j + 1)
+                       for j in range(r)], dim=1)
+    full = gather_sigma(sig, total)
+    if rank == 0:
+        q.put(full.numpy())
+    dist.destroy_process_group()
+
+
+def test_gather_sigma_world2_gloo():
+    n, m, r = 7, 6, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(g, 2, port, n, m, r, q)) for g in range(2)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = engine.half_grid_count(n, m)
+    expect = np.stack([np.arange(total) / (j + 1) for j in range(r)], axis=1)
+    assert np.array_equal(full, expect)
+    # spectrum assembly rule: every non-self-conjugate representative twice
+    rep_of, _ = engine.partner_map(n, m)
+    values = np.sort(full[rep_of].ravel())[::-1]
+    assert len(values) == n * m * r

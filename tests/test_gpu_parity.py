@@ -1,0 +1,346 @@
+"""GPU parity of the CUDA path against the reference (golden vectors made by
+the reference itself, tests/golden/make_golden.py) and the CPU oracle.
+
+Tolerances are the north-star bar: per frequency
+max_j |sigma - sigma_ref| / sigma_ref[f,0] <= 1e-5 in fp32 and <= 1e-10 in
+fp64; the reference's own unit-test tolerances where those are tighter
+(pkg/tests/test_symbol.py, test_blocksvd.py, test_acceptance.py).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2506_05617_b200 as cs
+from paper_2506_05617_b200 import configs, engine
+
+from conftest import averaging_symbol, identity_kernel, per_freq_rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 1e-5
+TOL64 = 1e-10
+
+
+def _kernel_from_golden(golden, name):
+    co, ci, kh, kw, seed, n, m = golden[f"sym_{name}_shape"]
+    return cs.random_kernel(int(co), int(ci), int(kh), int(kw), seed=int(seed)), cs.SpatialDims(int(n), int(m))
+
+
+# ---------------------------------------------------------------- K1 symbol
+@pytest.mark.parametrize("name", ["a", "b", "c", "d"])
+def test_symbol_field_f64_matches_reference(cuda, golden, name):
+    kernel, dims = _kernel_from_golden(golden, name)
+    fld = cs.build_symbol_field(kernel, dims)
+    ref = golden[f"sym_{name}_blocks"]
+    assert fld.blocks.shape == ref.shape
+    # pkg/tests/test_symbol.py:53-59 uses atol 1e-13
+    assert np.abs(fld.blocks - ref).max() <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["a", "b", "c", "d"])
+def test_symbol_field_f32_matches_reference(cuda, golden, name):
+    kernel, dims = _kernel_from_golden(golden, name)
+    fld = cs.build_symbol_field(kernel, dims, dtype="f32")
+    ref = golden[f"sym_{name}_blocks"]
+    assert np.abs(fld.blocks - ref).max() <= 2e-6 * np.abs(ref).max()
+
+
+def test_symbol_at_closed_form(cuda):
+    avg = cs.ConvKernel.from_array(np.full((1, 1, 3, 3), 1.0 / 9.0))
+    for k1 in (0.0, 0.25, 0.5, 1 / 3):
+        for k2 in (0.0, 0.5, 0.75):
+            got = cs.symbol_at(avg, (k1, k2))
+            assert got.shape == (1, 1)
+            assert abs(got[0, 0] - averaging_symbol(k1, k2)) < 1e-14
+
+
+def test_symbol_tap_sum_at_zero(cuda):
+    kernel = cs.random_kernel(3, 2, 3, 4, seed=5)
+    got = cs.symbol_at(kernel, (0.0, 0.0))
+    assert np.allclose(got, kernel.weights.sum(axis=(2, 3)), atol=1e-14)
+    assert np.abs(got.imag).max() < 1e-14
+
+
+@pytest.mark.parametrize("dt,tol", [("f32", 2e-6), ("f64", 1e-13)])
+@pytest.mark.parametrize("shape", [(64, 64, 3, 64, 64), (8, 5, 5, 7, 6), (3, 7, 4, 5, 9), (16, 16, 1, 4, 1)])
+def test_half_grid_symbol_vs_oracle(cuda, orc, dt, tol, shape):
+    co, ci, k, n, m = shape
+    w = configs.layer_weights(configs.LayerSpec(co, ci, k, n, m, 7))
+    kernel = cs.ConvKernel.from_array(w if dt == "f32" else w.astype(np.float64))
+    wd = engine.weights_to_device(kernel, dt, cuda)
+    half = engine.symbol_field(wd, n, m, dt, half=True).cpu().numpy()
+    reps = engine.half_grid_indices(n, m)
+    ref = orc.symbol_field(w.astype(np.float64), n, m)[reps]
+    assert half.shape == ref.shape
+    assert np.abs(half - ref).max() <= tol * max(1.0, np.abs(ref).max())
+    # a sub-range of representatives lands at the same place
+    u0, cnt = len(reps) // 3, max(1, len(reps) // 4)
+    part = engine.symbol_field(wd, n, m, dt, half=True, f_first=u0, f_count=cnt).cpu().numpy()
+    assert np.array_equal(part, half[u0:u0 + cnt])
+
+
+def test_full_grid_is_exact_conj_mirror(cuda):
+    kernel = cs.random_kernel(4, 3, 3, 3, seed=9)
+    n, m = 6, 5
+    fld = cs.build_symbol_field(kernel, cs.SpatialDims(n, m))
+    b = fld.blocks
+    for f in range(n * m):
+        i, j = divmod(f, m)
+        fs = ((n - i) % n) * m + (m - j) % m
+        assert np.array_equal(b[fs], np.conj(b[f]))
+
+
+def test_layouts_hold_identical_bits(cuda):
+    kernel = cs.random_kernel(2, 2, 3, 3, seed=9)
+    dims = cs.SpatialDims(n=6, m=5)
+    a = cs.build_symbol_field(kernel, dims, layout=cs.BLOCK_CONTIGUOUS)
+    b = cs.build_symbol_field(kernel, dims, layout=cs.FREQUENCY_STRIDED)
+    assert a.blocks.flags.c_contiguous and not b.blocks.flags.c_contiguous
+    assert np.array_equal(a.blocks, np.asarray(b.blocks))
+    assert np.array_equal(a.blocks, cs.convert_layout(b, cs.BLOCK_CONTIGUOUS).blocks)
+
+
+def test_strided_kernel_layout_matches(cuda):
+    kernel = cs.random_kernel(3, 4, 3, 3, seed=2)
+    wd = engine.weights_to_device(kernel, "f64", cuda)
+    a = engine.symbol_field(wd, 5, 4, "f64", half=False).cpu().numpy()
+    b = engine.symbol_field(wd, 5, 4, "f64", half=False, layout=1).cpu().numpy()
+    assert np.abs(a - b.transpose(2, 0, 1)).max() <= 1e-14
+
+
+# ---------------------------------------------------------------- K2/K3 SVD
+@pytest.mark.parametrize("idx", range(4))
+def test_oracle_fixtures_f64(cuda, golden, idx):
+    n, m, c_in, c_out, seed = (int(v) for v in golden[f"fix{idx}_shape"])
+    kernel = cs.random_kernel(c_out, c_in, 3, 3, seed=seed)
+    dims = cs.SpatialDims(n=n, m=m)
+    vals = cs.compute_spectrum(kernel, dims).values
+    assert len(vals) == n * m * min(c_in, c_out)
+    ref = golden[f"fix{idx}_values"]
+    assert np.abs(vals - ref).max() <= TOL64 * ref[0]
+    # the reference's acceptance criterion against the dense explicit SVD
+    assert np.allclose(vals, golden[f"fix{idx}_dense"], rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_oracle_fixtures_f32(cuda, golden, idx):
+    n, m, c_in, c_out, seed = (int(v) for v in golden[f"fix{idx}_shape"])
+    kernel = cs.random_kernel(c_out, c_in, 3, 3, seed=seed)
+    dims = cs.SpatialDims(n=n, m=m)
+    fld = cs.build_symbol_field(kernel, dims, dtype="f32", return_device_tensors=True)
+    res, trip = cs.spectrum_from_field(fld, values_only=False)
+    sig = np.array([np.asarray(t.sigma) for t in trip])
+    assert per_freq_rel_err(sig, golden[f"fix{idx}_sigma"]).max() <= TOL32
+
+
+def test_cfg1_full_f32(cuda, golden):
+    layer = configs.WORKLOADS[1].layers[0]
+    w = configs.layer_weights(layer)
+    res = cs.compute_spectrum(cs.ConvKernel.from_array(w), cs.SpatialDims(layer.n, layer.m))
+    ref = golden["cfg1_l0_values"]
+    assert len(res.values) == 16 * 1024
+    assert np.abs(res.values - ref).max() <= TOL32 * ref[0]
+
+
+def test_cfg1_per_frequency_f32_and_f64(cuda, golden):
+    layer = configs.WORKLOADS[1].layers[0]
+    w = configs.layer_weights(layer)
+    ref = golden["cfg1_l0_sigma"]
+    for dt, tol in (("f32", TOL32), ("f64", TOL64)):
+        kernel = cs.ConvKernel.from_array(w if dt == "f32" else w.astype(np.float64))
+        fld = cs.build_symbol_field(kernel, cs.SpatialDims(layer.n, layer.m), dtype=dt,
+                                    return_device_tensors=True)
+        _, trip = cs.spectrum_from_field(fld, values_only=False)
+        sig = np.array([np.asarray(t.sigma) for t in trip])
+        assert per_freq_rel_err(sig, ref).max() <= tol, dt
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_svd_block_matches_reference(cuda, golden, i):
+    A = golden[f"blk{i}_A"]
+    t = cs.svd_block(A)
+    assert np.abs(t.sigma - golden[f"blk{i}_sigma"]).max() <= 1e-10 * golden[f"blk{i}_sigma"][0]
+    r = min(A.shape)
+    assert t.U.shape == (A.shape[0], r) and t.V.shape == (A.shape[1], r)
+    assert np.allclose(t.U.conj().T @ t.U, np.eye(r), atol=1e-10)
+    assert np.allclose(t.V.conj().T @ t.V, np.eye(r), atol=1e-10)
+    assert list(t.sigma) == sorted(t.sigma, reverse=True)
+    recon = t.U @ np.diag(t.sigma) @ t.V.conj().T
+    assert np.linalg.norm(recon - A) <= 1e-10 * max(1.0, np.linalg.norm(A))
+
+
+def test_identity_and_scalar_blocks(cuda):
+    t = cs.svd_block(np.eye(2, dtype=complex))
+    assert np.allclose(t.sigma, [1.0, 1.0], atol=1e-14)
+    t = cs.svd_block(np.array([[-1 / 3]], dtype=complex))
+    assert abs(t.sigma[0] - 1 / 3) < 1e-16
+    assert np.allclose(t.U * t.sigma[0] * np.conj(t.V), -1 / 3)
+
+
+def test_zero_block_keeps_orthonormal_factors(cuda):
+    t = cs.svd_block(np.zeros((3, 2), dtype=complex))
+    assert np.allclose(t.sigma, 0.0)
+    assert np.allclose(t.U.conj().T @ t.U, np.eye(2), atol=1e-12)
+
+
+def test_rank_deficient_block(cuda):
+    rng = np.random.default_rng(2)
+    col = rng.standard_normal((4, 1)) + 1j * rng.standard_normal((4, 1))
+    rng = np.random.default_rng(3)
+    other = rng.standard_normal((4, 1)) + 1j * rng.standard_normal((4, 1))
+    t = cs.svd_block(np.hstack([col, 2 * col, other]))
+    assert t.sigma[2] < 1e-12 * t.sigma[0]
+    assert np.allclose(t.U.conj().T @ t.U, np.eye(3), atol=1e-9)
+
+
+def test_identity_kernel_all_ones(cuda):
+    for dims in (cs.SpatialDims(4, 4), cs.SpatialDims(16, 16), cs.SpatialDims(7, 5)):
+        vals = cs.compute_spectrum(identity_kernel(3), dims).values
+        assert len(vals) == 3 * dims.size
+        assert np.max(np.abs(vals - 1.0)) <= 1e-12
+
+
+def test_averaging_2x2(cuda):
+    avg = cs.ConvKernel.from_array(np.full((1, 1, 3, 3), 1.0 / 9.0))
+    vals = cs.compute_spectrum(avg, cs.SpatialDims(2, 2)).values
+    assert np.max(np.abs(vals - np.array([1.0, 1 / 3, 1 / 3, 1 / 9]))) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_parseval(cuda, seed):
+    kernel = cs.random_kernel(4, 3, 3, 3, seed=seed)
+    dims = cs.SpatialDims(n=6, m=5)
+    vals = cs.compute_spectrum(kernel, dims).values
+    expected = dims.size * np.sum(kernel.weights ** 2)
+    assert abs(np.sum(vals ** 2) - expected) <= 1e-8 * expected
+
+
+def test_scaling_by_alpha(cuda):
+    kernel = cs.random_kernel(2, 2, 3, 3, seed=14)
+    dims = cs.SpatialDims(4, 4)
+    base = cs.compute_spectrum(kernel, dims).values
+    scaled = cs.compute_spectrum(cs.ConvKernel.from_array(2.5 * kernel.weights), dims).values
+    assert np.allclose(scaled, 2.5 * base, rtol=1e-12, atol=0)
+
+
+def test_shift_and_flip_invariance(cuda):
+    base = cs.random_kernel(2, 2, 3, 3, seed=3)
+    padded = np.zeros((2, 2, 4, 3))
+    padded[:, :, 0:3, :] = base.weights
+    dims = cs.SpatialDims(n=4, m=6)
+    sa = cs.compute_spectrum(base, dims).values
+    sb = cs.compute_spectrum(cs.ConvKernel.from_array(padded), dims).values
+    assert np.allclose(sa, sb, rtol=1e-12, atol=0)
+    base = cs.random_kernel(3, 2, 3, 3, seed=4)
+    flipped = cs.ConvKernel.from_array(base.weights[:, :, ::-1, ::-1])
+    dims = cs.SpatialDims(n=5, m=4)
+    assert np.allclose(cs.compute_spectrum(base, dims).values,
+                       cs.compute_spectrum(flipped, dims).values, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_values_only_matches_full_bitwise(cuda, dt):
+    kernel = cs.random_kernel(3, 2, 3, 3, seed=15)
+    fld = cs.build_symbol_field(kernel, cs.SpatialDims(5, 4), dtype=dt)
+    only = cs.spectrum_from_field(fld, values_only=True)
+    full, trip = cs.spectrum_from_field(fld, values_only=False)
+    assert np.array_equal(only.values, full.values)
+    assert len(trip) == 20
+
+
+def test_worker_count_does_not_change_bits(cuda):
+    kernel = cs.random_kernel(3, 3, 3, 3, seed=16)
+    fld = cs.build_symbol_field(kernel, cs.SpatialDims(8, 8))
+    v = [cs.spectrum_from_field(fld, workers=w).values for w in (1, 2, 0)]
+    assert np.array_equal(v[0], v[1]) and np.array_equal(v[0], v[2])
+
+
+@pytest.mark.parametrize("shape", [(2, 3), (3, 2), (5, 5)])
+def test_full_mode_triplets_reconstruct_blocks(cuda, shape):
+    kernel = cs.random_kernel(shape[0], shape[1], 3, 3, seed=17)
+    fld = cs.build_symbol_field(kernel, cs.SpatialDims(3, 3))
+    _, trip = cs.spectrum_from_field(fld, values_only=False)
+    for f, t in enumerate(trip):
+        recon = t.U @ np.diag(t.sigma) @ t.V.conj().T
+        assert np.allclose(recon, fld.blocks[f], atol=1e-10)
+        r = min(shape)
+        assert np.allclose(t.U.conj().T @ t.U, np.eye(r), atol=1e-10)
+        assert np.allclose(t.V.conj().T @ t.V, np.eye(r), atol=1e-10)
+
+
+def test_nan_block_raises(cuda):
+    with pytest.raises(cs.ConvergenceFailure):
+        cs.svd_block(np.full((3, 3), np.nan, dtype=complex))
+
+
+def test_nan_field_reports_frequency(cuda):
+    fld = cs.build_symbol_field(cs.random_kernel(2, 2, 3, 3, seed=20), cs.SpatialDims(3, 3))
+    fld.blocks[4] = np.nan
+    with pytest.raises(cs.ConvergenceFailure) as err:
+        cs.spectrum_from_field(fld)
+    assert "frequency index 4" in str(err.value)
+    fld = cs.build_symbol_field(cs.random_kernel(2, 2, 3, 3, seed=20), cs.SpatialDims(3, 3))
+    fld.blocks[8] = np.nan  # a partner frequency: must not be hidden by the half grid
+    with pytest.raises(cs.ConvergenceFailure) as err:
+        cs.spectrum_from_field(fld)
+    assert "frequency index 8" in str(err.value)
+
+
+def test_reference_built_field_accepted(cuda, golden):
+    # a field straight from the reference (not bitwise conj-symmetric) is solved per block
+    kernel, dims = _kernel_from_golden(golden, "c")
+    fld = cs.SymbolField(grid=cs.FrequencyGrid(dims), blocks=golden["sym_c_blocks"])
+    ours = cs.spectrum_from_field(cs.build_symbol_field(kernel, dims)).values
+    theirs = cs.spectrum_from_field(fld).values
+    assert np.abs(ours - theirs).max() <= 1e-12 * ours[0]
+
+
+def test_max_sweeps_one_fails(cuda):
+    kernel = cs.random_kernel(4, 4, 3, 3, seed=1)
+    with pytest.raises(cs.ConvergenceFailure) as err:
+        cs.compute_spectrum(kernel, cs.SpatialDims(4, 4), max_sweeps=1)
+    assert "frequency index" in str(err.value)
+
+
+def _periodic_matrix(weights, n, m):
+    """Dense unrolled periodic convolution, index (x1*n + x2)*c + ch
+    (restates pkg/src/convspectra/explicit.py:67-128 for small test sizes)."""
+    co, ci, kh, kw = weights.shape
+    A = np.zeros((n * m * co, n * m * ci))
+    for x1 in range(m):
+        for x2 in range(n):
+            for p in range(kh):
+                for q in range(kw):
+                    y1, y2 = (x1 + p - kh // 2) % m, (x2 + q - kw // 2) % n
+                    r0, c0 = (x1 * n + x2) * co, (y1 * n + y2) * ci
+                    A[r0:r0 + co, c0:c0 + ci] += weights[:, :, p, q]
+    return A
+
+
+def test_singular_vector_residual(cuda):
+    # pkg/tests/test_acceptance.py:122-136: ||A v - sigma u|| <= 1e-8 for all 16 frequencies
+    kernel = cs.random_kernel(2, 2, 3, 3, seed=300)
+    dims = cs.SpatialDims(4, 4)
+    fld = cs.build_symbol_field(kernel, dims)
+    _, trip = cs.spectrum_from_field(fld, values_only=False)
+    A = _periodic_matrix(kernel.weights, 4, 4)
+    dense = np.sort(np.linalg.svd(A, compute_uv=False))[::-1]
+    vals = cs.spectrum_from_field(fld).values
+    assert np.allclose(vals, dense, rtol=1e-6, atol=0)
+    for t in trip:
+        for col in range(len(t.sigma)):
+            v = cs.materialize_singular_vector(t, col, "right", dims)
+            u = cs.materialize_singular_vector(t, col, "left", dims)
+            assert np.linalg.norm(A @ v - t.sigma[col] * u) <= 1e-8
+
+
+def test_materialize_orthonormal_and_range(cuda):
+    kernel = cs.random_kernel(3, 3, 3, 3, seed=18)
+    dims = cs.SpatialDims(4, 4)
+    _, trip = cs.spectrum_from_field(cs.build_symbol_field(kernel, dims), values_only=False)
+    vecs = [cs.materialize_singular_vector(trip[5], c, "right", dims) for c in range(3)]
+    for a in range(3):
+        for b in range(3):
+            assert abs(np.vdot(vecs[a], vecs[b]) - (1.0 if a == b else 0.0)) < 1e-10
+    with pytest.raises(cs.IndexOutOfRange):
+        cs.materialize_singular_vector(trip[0], 3, "left", dims)
