@@ -94,6 +94,33 @@ int cs_batched_svd(const void *blocks, int dtype, long long count, int c_out, in
                    void *V, int *info, int *zero_sigma, void *workspace,
                    size_t workspace_bytes, void *stream);
 
+/* Which kernel family the planner picks for a batch: 2 = panel (cluster,
+ * register-resident), 0 = row-split fast kernel, 1 = generic; -1 = invalid. */
+int cs_batched_svd_plan_kind(int dtype, long long count, int c_out, int c_in,
+                             int want_vectors);
+
+/* Indexed / warm-started variant (panel kernel only).  Batch item i solves
+ * matrix index[i] of `blocks` (outputs are written at index[i] as well); with
+ * init_X it starts from X = init_X[i] ((mr, nc) row-major, working
+ * orientation X = A or A^H) instead of the block, and with init_V from
+ * V = init_V[init_V_index[i]] ((nc, nc) row-major) instead of the identity.
+ * Same algorithm, tolerance and outputs as cs_batched_svd. */
+int cs_batched_svd_indexed(const void *blocks, int dtype, long long count, int c_out,
+                           int c_in, int want_vectors, double tol, int max_sweeps,
+                           const long long *index, const void *init_X, const void *init_V,
+                           const long long *init_V_index, void *sigma, void *U, void *V,
+                           int *info, int *zero_sigma, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
+/* Warm-start GEMM: out_X[i] = X_{warm_ids[i]} . Vw[seed_ids[i]] where X_f is
+ * the working matrix of block f (A_f, or A_f^H when c_out < c_in) and Vw the
+ * (nc, nc) working-orientation right factors of already solved blocks (the V
+ * output for tall blocks, the U output for wide ones).  No reference
+ * counterpart: the reference solves every frequency from scratch. */
+int cs_warm_start_gemm(const void *blocks, int dtype, int c_out, int c_in, long long count,
+                       const long long *warm_ids, const long long *seed_ids, const void *Vw,
+                       void *out_X, void *stream);
+
 /* Heterogeneous batch in one call (cfg4: 16 layers, 4 shapes).  `groups` is a
  * HOST array; each group is solved like cs_batched_svd; groups run
  * concurrently on forked streams joined back into `stream`. */

@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "cs_jacobi.cuh"
+#include "cs_panel.cuh"
 
 namespace cs {
 
@@ -100,6 +101,51 @@ static bool plan_fast(int co, int ci, bool wantv, int C, JacShape &s) {
     return s.smem <= JAC_SMEM_LIMIT;
 }
 
+// Panel kernel (cs_panel.cuh): 2C column panels of w columns, whole columns
+// of [X; V] per CTA; a-panel rows in registers, b panel (x2 when C > 1 for
+// the cluster rotation) + a staging copy of the a panel in shared memory.
+template <typename T>
+static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
+    base_shape(co, ci, wantv, C, s);
+    s.kind = 2;
+    s.ncp = ((s.nc + 4 * C - 1) / (4 * C)) * (4 * C);
+    const int w = s.ncp / (2 * C);
+    if (w > JAC_MAX_THREADS) return false;
+    s.P = w;
+    s.R = s.mr;
+    s.Rv = wantv ? s.nc : 0;
+    int G = 1;
+    while (G * 2 <= 32 && w * G * 2 <= JAC_MAX_THREADS && G * 2 * 4 <= pow2ceil(s.mr)) G *= 2;
+    const int rplx = std::max(2, pow2ceil((s.mr + G - 1) / G));
+    const int rplv = wantv ? rplx : 0;
+    const int budget = sizeof(T) == 4 ? 16 : 8;  // complex rows per column held in registers
+    if (rplx + rplv > budget) return false;
+    s.G = G;
+    s.RPL = rplx;
+    s.threads = ((w * G + 31) / 32) * 32;
+    const int T2sz = 2 * sizeof(T);
+    s.ldv = G * rplx;  // row offset of the V rows in a column
+    s.ldx = pad_ld(G * (rplx + rplv), G, T2sz);
+    size_t off = 0;
+    s.off_sig = off;
+    off = align16(off + s.ncp * sizeof(T));
+    s.off_perm = off;
+    off = align16(off + 2 * s.ncp * sizeof(int));
+    s.off_send = off;  // staging for the cluster norm gather
+    off = align16(off + s.ncp * sizeof(T));
+    s.off_recv = s.off_mbar = off;  // sweep flags + panel position tables
+    off = align16(off + (4 + 64) * sizeof(int));
+    s.off_x = off;
+    const size_t panel = (size_t)w * s.ldx * T2sz;
+    off = align16(off + panel);
+    s.off_v = off;
+    off = align16(off + panel * (C > 1 ? 2 : 1));
+    s.smem = off;
+    s.smem_resident = 1;
+    s.nbuf = 1;
+    return s.smem <= JAC_SMEM_LIMIT;
+}
+
 template <typename T>
 static bool plan_generic(int co, int ci, bool wantv, int C, bool smem_resident, JacShape &s) {
     base_shape(co, ci, wantv, C, s);
@@ -145,6 +191,16 @@ template <typename T>
 static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     const int Cs[5] = {1, 2, 4, 8, 16};
     for (int i = 0; i < 5; ++i) {
+        if (!plan_panel<T>(co, ci, wantv, Cs[i], s)) continue;
+        int j = i;
+        while (j < 4 && count * Cs[j] < 2LL * num_sms()) {
+            JacShape t;
+            if (!plan_panel<T>(co, ci, wantv, Cs[j + 1], t) || t.P < 4) break;
+            ++j;
+        }
+        return plan_panel<T>(co, ci, wantv, Cs[j], s);
+    }
+    for (int i = 0; i < 5; ++i) {
         if (!plan_fast<T>(co, ci, wantv, Cs[i], s)) continue;
         // few matrices: spread each over more SMs while rows per CTA stay >= 16
         int j = i;
@@ -187,10 +243,19 @@ static int svd_workspace(long long count, int co, int ci, bool wantv, size_t *by
 template <typename T>
 static int svd_run(const void *blocks, long long count, int co, int ci, bool wantv, double tol,
                    int max_sweeps, void *sigma, void *U, void *V, int *info, int *zero_sigma,
-                   void *ws, size_t ws_bytes, cudaStream_t st) {
+                   void *ws, size_t ws_bytes, cudaStream_t st, const long long *index = nullptr,
+                   const void *initX = nullptr, const void *initV = nullptr,
+                   const long long *initV_index = nullptr) {
     if (count == 0) return CS_OK;
     JacArgs<T> a = {};
     if (!plan<T>(co, ci, wantv, count, a.s)) return fail(CS_EINVAL, "batched SVD: no plan");
+    if ((index || initX || initV) && a.s.kind != 2)
+        return fail(CS_EINVAL, "batched SVD: indexed / warm-started solves need the panel kernel");
+    if (initV && !(wantv && initV_index)) return fail(CS_EINVAL, "batched SVD: initV needs vectors and an index");
+    a.index = index;
+    a.initX = (const cplx_t<T> *)initX;
+    a.initV = (const cplx_t<T> *)initV;
+    a.initV_index = initV_index;
     a.blocks = (const cplx_t<T> *)blocks;
     a.count = count;
     a.co = co;
@@ -251,6 +316,37 @@ extern "C" int cs_batched_svd(const void *blocks, int dtype, long long count, in
                               zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream);
     return svd_run<double>(blocks, count, c_out, c_in, wv, tol, max_sweeps, sigma, U, V, info,
                            zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int cs_batched_svd_plan_kind(int dtype, long long count, int c_out, int c_in,
+                                        int want_vectors) {
+    if (check_svd_args(dtype, count, c_out, c_in, 1)) return -1;
+    JacShape s;
+    const bool ok = dtype == CS_F32 ? plan<float>(c_out, c_in, want_vectors != 0, std::max(count, 1LL), s)
+                                    : plan<double>(c_out, c_in, want_vectors != 0, std::max(count, 1LL), s);
+    return ok ? s.kind : -1;
+}
+
+extern "C" int cs_batched_svd_indexed(const void *blocks, int dtype, long long count, int c_out,
+                                      int c_in, int want_vectors, double tol, int max_sweeps,
+                                      const long long *index, const void *init_X,
+                                      const void *init_V, const long long *init_V_index,
+                                      void *sigma, void *U, void *V, int *info, int *zero_sigma,
+                                      void *workspace, size_t workspace_bytes, void *stream) {
+    int st = check_svd_args(dtype, count, c_out, c_in, max_sweeps);
+    if (st) return st;
+    if (count && (!sigma || !info || (!blocks && !init_X)))
+        return fail(CS_EINVAL, "batched SVD: null pointer");
+    if (want_vectors && count && (!U || !V))
+        return fail(CS_EINVAL, "batched SVD: U and V required with want_vectors");
+    const bool wv = want_vectors != 0;
+    if (dtype == CS_F32)
+        return svd_run<float>(blocks, count, c_out, c_in, wv, tol, max_sweeps, sigma, U, V, info,
+                              zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream, index,
+                              init_X, init_V, init_V_index);
+    return svd_run<double>(blocks, count, c_out, c_in, wv, tol, max_sweeps, sigma, U, V, info,
+                           zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream, index,
+                           init_X, init_V, init_V_index);
 }
 
 extern "C" size_t cs_batched_svd_grouped_workspace(const cs_svd_group *groups, int num_groups,

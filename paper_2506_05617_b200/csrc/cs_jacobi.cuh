@@ -59,6 +59,13 @@ template <typename T> struct JacArgs {
     cplx_t<T> *Vw;  // factor with nc rows
     int *info, *zero_sigma;
     cplx_t<T> *scratch;
+    // warm start (panel kernel only): batch item i solves matrix index[i]
+    // (outputs land there too), starting from X = initX[i] (mr x nc, working
+    // orientation) and V = initV[initV_index[i]] (nc x nc) instead of (A, I)
+    const long long *index;
+    const cplx_t<T> *initX;
+    const cplx_t<T> *initV;
+    const long long *initV_index;
 };
 
 // ---------------------------------------------------------------------------
@@ -131,14 +138,16 @@ __device__ __forceinline__ void pair_cols(int k, int r, int ncp, int &p, int &q)
 
 template <typename T> struct Rot { T cm1, wr, wi; };
 
-// 0: skip, 1: rotate (params in R), -1: non-finite input
+// 0: skip, 1: rotate (params in R), -1: non-finite input.
+// The skip test compares squares (|gamma|^2 <= tol^2 alpha beta), so most
+// late-sweep pairs cost no sqrt at all.
 template <typename T>
 __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> &R) {
     if (!(dfinite(al) && dfinite(be) && dfinite(gr) && dfinite(gi))) return -1;
     if (al == (T)0 || be == (T)0) return 0;
     const T q = gr * gr + gi * gi;
-    const T ag = (q > (T)1e-30) ? dsqrt(q) : dhypot(gr, gi);
-    if (ag <= tol * dsqrt(al * be)) return 0;
+    if (q <= tol * tol * (al * be)) return 0;
+    const T ag = dsqrt(q);
     const T d = be - al, g = (T)2 * ag;
     T t = g / (fabs(d) + dhypot(d, g));
     if (d < (T)0) t = -t;
@@ -147,6 +156,39 @@ __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> 
     const T s = t / r;
     R.wr = s * (gr / ag);
     R.wi = s * (gi / ag);
+    return 1;
+}
+
+// fp32: MUFU rsqrt + one Newton step and __fdividef -- no IEEE div/sqrt
+// slow-path subroutine calls (whose calling convention forced register
+// spills in the hot loop).  A relative error e in r = sqrt(1+t^2) makes the
+// (c-1)-form rotation non-unitary by only ~e*t^2, so small late-sweep
+// rotations stay unitary to storage precision.
+__device__ __forceinline__ float nr_rsqrt(float x) {
+    const float y = rsqrtf(x);
+    return y * fmaf(-0.5f * x * y, y, 1.5f);
+}
+template <>
+__device__ __forceinline__ int rot_params<float>(float al, float be, float gr, float gi, float tol,
+                                                 Rot<float> &R) {
+    if (!(isfinite(al) && isfinite(be) && isfinite(gr) && isfinite(gi))) return -1;
+    if (al == 0.f || be == 0.f) return 0;
+    const float q = gr * gr + gi * gi;
+    if (q <= tol * tol * (al * be)) return 0;
+    const float inv_ag = nr_rsqrt(q);
+    const float ag = q * inv_ag;
+    const float d = be - al, g = 2.f * ag;
+    const float h2 = fmaf(d, d, g * g);
+    const float hyp = h2 * nr_rsqrt(h2);
+    float t = __fdividef(g, fabsf(d) + hyp);
+    if (d < 0.f) t = -t;
+    const float r2 = fmaf(t, t, 1.f);
+    const float ir = nr_rsqrt(r2);
+    const float r = r2 * ir;
+    R.cm1 = -(t * t) * __fdividef(ir, 1.f + r);
+    const float s = t * ir;
+    R.wr = s * gr * inv_ag;
+    R.wi = s * gi * inv_ag;
     return 1;
 }
 

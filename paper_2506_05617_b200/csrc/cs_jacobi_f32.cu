@@ -1,5 +1,6 @@
 // cs_jacobi_f32.cu -- float instantiations of the batched Jacobi kernels (see cs_jacobi.cuh).
 #include "cs_jacobi.cuh"
+#include "cs_panel.cuh"
 
 namespace cs {
 
@@ -25,6 +26,26 @@ static int fast_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry
     return fail(CS_EINVAL, "batched SVD: unsupported rows per lane");
 }
 
+template <int C_, int RPL_>
+static int panel_rpl(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
+    if constexpr (2 * RPL_ <= 16)
+        if (wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_>, a, st, dry, ncl);
+    if constexpr (RPL_ <= 16)
+        if (!wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, 0>, a, st, dry, ncl);
+    return fail(CS_EINVAL, "batched SVD: panel rows per lane exceed the register budget");
+}
+
+template <int C_>
+static int panel_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
+    switch (a.s.RPL) {
+        case 2: return panel_rpl<C_, 2>(a, wantv, st, dry, ncl);
+        case 4: return panel_rpl<C_, 4>(a, wantv, st, dry, ncl);
+        case 8: return panel_rpl<C_, 8>(a, wantv, st, dry, ncl);
+        case 16: return panel_rpl<C_, 16>(a, wantv, st, dry, ncl);
+    }
+    return fail(CS_EINVAL, "batched SVD: unsupported panel rows per lane");
+}
+
 template <int C_>
 static int generic_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
     if (a.s.smem_resident) {
@@ -36,7 +57,15 @@ static int generic_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool 
 }
 
 int jacobi_dispatch_f32(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
-    if (a.s.kind == 0) {
+    if (a.s.kind == 2) {
+        switch (a.s.C) {
+            case 1: return panel_c<1>(a, wantv, st, dry, ncl);
+            case 2: return panel_c<2>(a, wantv, st, dry, ncl);
+            case 4: return panel_c<4>(a, wantv, st, dry, ncl);
+            case 8: return panel_c<8>(a, wantv, st, dry, ncl);
+            case 16: return panel_c<16>(a, wantv, st, dry, ncl);
+        }
+    } else if (a.s.kind == 0) {
         switch (a.s.C) {
             case 1: return fast_c<1>(a, wantv, st, dry, ncl);
             case 2: return fast_c<2>(a, wantv, st, dry, ncl);

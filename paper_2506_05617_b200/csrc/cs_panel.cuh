@@ -1,0 +1,520 @@
+// cs_panel.cuh -- K3: panel-blocked one-sided Jacobi for a cluster of C CTAs.
+//
+// Same rotation, tolerance and convergence rule as cs_jacobi.cuh (the
+// reference's blocksvd.py:75-125 semantics); what changes is WHERE the data
+// lives and hence which pair ordering is used.
+//
+// Data: the augmented working matrix [X; V] (mr + nc rows when vectors are
+// requested, mr otherwise) has its ncp columns split into 2C panels of w
+// columns.  CTA c of the cluster owns two whole panels ("a" and "b"), all
+// rows -- so every (alpha, beta, gamma) reduction is local to one CTA
+// (registers + warp shuffles), never across the cluster.  On B200 the
+// cluster fabric moves only ~20 B/cycle/SM with ~300-cycle latency
+// (tools/dsmem_bench.cu), so a per-round cross-CTA reduction cost more than
+// the round itself; here the cluster exchanges whole panels only between
+// super-rounds (once per w rounds), by per-thread DSMEM loads.
+//
+// Ordering (a block version of the circle method, every pair once per sweep):
+//   sweep = [within-panel rounds: w-1 rounds, circle method inside each of
+//            the CTA's two panels]
+//         + 2C-1 super-rounds, each [w cross rounds a x b] followed (except
+//           the last) by a panel rotation across the cluster (circle method
+//           over 2C panel positions; position 0 never moves).
+//   In cross round s, pair slot k rotates a_k (stationary: its rows live in
+//   the slot's registers for the whole super-round) with b_{(k+s) mod w}
+//   (read from and written back to shared memory).  w-1 + (2C-1) w = ncp-1
+//   rounds of w pairs = all ncp(ncp-1)/2 pairs.
+// Thread layout: slot k = tid / G (k < w), lane g = tid % G owns X rows
+// g + G*i (i < RPLX) and V rows g + G*i (i < RPLV) of its two columns.
+#pragma once
+
+#include "cs_jacobi.cuh"
+
+namespace cs {
+
+// owner CTA of panel position p (CTA c holds positions c and 2C-1-c)
+__device__ __forceinline__ int pos_owner(int p, int C) { return p < C ? p : 2 * C - 1 - p; }
+
+// 32-bit shared-memory accessors.  The hot loops walk a column with an
+// opaque pointer bump (asm "+r") so the compiler keeps ONE live address per
+// column instead of hoisting RPL runtime-strided addresses into registers.
+template <typename T> struct SmemIO;
+template <> struct SmemIO<float> {
+    static __device__ __forceinline__ float2 ld(uint32_t a) {
+        float2 v;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+        return v;
+    }
+    static __device__ __forceinline__ void st(uint32_t a, float2 v) {
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+    }
+};
+template <> struct SmemIO<double> {
+    static __device__ __forceinline__ double2 ld(uint32_t a) {
+        double2 v;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+        return v;
+    }
+    static __device__ __forceinline__ void st(uint32_t a, double2 v) {
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+    }
+};
+
+// call-free sqrt / quotient for the fp32 epilogue (IEEE slow paths are
+// subroutine calls that cost spills in the whole kernel); fp64 stays IEEE
+__device__ __forceinline__ float epi_sqrt(float x) { return x > 0.f ? x * nr_rsqrt(x) : 0.f; }
+__device__ __forceinline__ double epi_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float epi_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double epi_div(double a, double b) { return a / b; }
+
+template <typename T, int N>
+__device__ __forceinline__ void col_load(cplx_t<T> (&v)[N], uint32_t addr, uint32_t stride) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        v[i] = SmemIO<T>::ld(addr);
+        addr += stride;
+        asm volatile("" : "+r"(addr));
+    }
+}
+template <typename T, int N>
+__device__ __forceinline__ void col_load_cluster(cplx_t<T> (&v)[N], uint32_t addr, uint32_t stride) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if constexpr (sizeof(T) == 4) {
+            asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v[i].x), "=f"(v[i].y) : "r"(addr) : "memory");
+        } else {
+            asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v[i].x), "=d"(v[i].y) : "r"(addr) : "memory");
+        }
+        addr += stride;
+        asm volatile("" : "+r"(addr));
+    }
+}
+template <typename T, int N>
+__device__ __forceinline__ void col_store(const cplx_t<T> (&v)[N], uint32_t addr, uint32_t stride) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        SmemIO<T>::st(addr, v[i]);
+        addr += stride;
+        asm volatile("" : "+r"(addr));
+    }
+}
+
+// within-panel rounds (w-1 rounds, circle method inside each of the CTA's two
+// panels, both columns from shared memory); records the squared column norms
+// of round 0 in sig2.  Returns bit0 = rotated, bit1 = non-finite.
+// __noinline__: the two phases are register-allocated separately.
+template <typename T, int C, int RPLX, int RPLV>
+__device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem, cplx_t<T> *Abuf,
+                                         cplx_t<T> *Bbuf, int start_a, int start_b, T tol) {
+    using T2 = cplx_t<T>;
+    constexpr bool WANTV = RPLV > 0;
+    constexpr int RPLV1 = WANTV ? RPLV : 1;
+    const int w = s.P, G = s.G, LD = s.ldx, VOFF = s.ldv;
+    const int tid = threadIdx.x, k = tid / G, g = tid % G;
+    const bool active = k < w;
+    constexpr uint32_t T2SZ = sizeof(T2);
+    const uint32_t rstride = (uint32_t)G * T2SZ;
+    const uint32_t voff_b = (uint32_t)VOFF * T2SZ;
+    const uint32_t colb = (uint32_t)LD * T2SZ;
+    T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
+    bool rot = false, bad = false;
+            {
+                const int hw = w / 2;
+                const int kk = k % hw;
+                T2 *panel = (k < hw) ? Abuf : Bbuf;
+                const int pid = (k < hw) ? start_a : start_b;
+#pragma unroll 1
+                for (int r = 0; r < w - 1; ++r) {
+                    int p = 0, q = 0;
+                    T2 x[RPLX], y[RPLX], xv[RPLV1], yv[RPLV1];
+                    T al = 0, be = 0, gr = 0, gi = 0;
+                    if (active) {
+                        pair_cols(kk, r, w, p, q);
+                        const uint32_t ap = smem_u32(panel) + p * colb + g * T2SZ;
+                        const uint32_t aq = smem_u32(panel) + q * colb + g * T2SZ;
+                        col_load<T, RPLX>(x, ap, rstride);
+                        col_load<T, RPLX>(y, aq, rstride);
+#pragma unroll
+                        for (int i = 0; i < RPLX; ++i) {
+                            al += x[i].x * x[i].x + x[i].y * x[i].y;
+                            be += y[i].x * y[i].x + y[i].y * y[i].y;
+                            gr += x[i].x * y[i].x + x[i].y * y[i].y;
+                            gi += x[i].x * y[i].y - x[i].y * y[i].x;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        if (off < G) {
+                            al += __shfl_xor_sync(0xffffffffu, al, off);
+                            be += __shfl_xor_sync(0xffffffffu, be, off);
+                            gr += __shfl_xor_sync(0xffffffffu, gr, off);
+                            gi += __shfl_xor_sync(0xffffffffu, gi, off);
+                        }
+                    }
+                    if (active) {
+                        if (r == 0 && g == 0) {
+                            sig2[pid * w + p] = al;
+                            sig2[pid * w + q] = be;
+                        }
+                        Rot<T> R;
+                        const int act = rot_params<T>(al, be, gr, gi, tol, R);
+                        if (act < 0) {
+                            bad = true;
+                        } else if (act > 0) {
+                            rot = true;
+                            const uint32_t ap = smem_u32(panel) + p * colb + g * T2SZ;
+                            const uint32_t aq = smem_u32(panel) + q * colb + g * T2SZ;
+#pragma unroll
+                            for (int i = 0; i < RPLX; ++i) rot_apply<T>(x[i], y[i], R);
+                            col_store<T, RPLX>(x, ap, rstride);
+                            col_store<T, RPLX>(y, aq, rstride);
+                            if constexpr (WANTV) {  // V rows only after the decision
+                                col_load<T, RPLV1>(xv, ap + voff_b, rstride);
+                                col_load<T, RPLV1>(yv, aq + voff_b, rstride);
+#pragma unroll
+                                for (int i = 0; i < RPLV; ++i) rot_apply<T>(xv[i], yv[i], R);
+                                col_store<T, RPLV1>(xv, ap + voff_b, rstride);
+                                col_store<T, RPLV1>(yv, aq + voff_b, rstride);
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+
+    return (rot ? 1 : 0) | (bad ? 2 : 0);
+}
+
+// 2C-1 super-rounds of cross pairs a x b: the a panel lives in registers, b
+// columns are read/written in shared memory; between super-rounds the panels
+// rotate across the cluster (DSMEM pulls).  The current b buffer index is
+// kept in flags[2].  Returns bit0 = rotated, bit1 = non-finite.
+template <typename T, int C, int RPLX, int RPLV>
+__device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, int rank,
+                                        cplx_t<T> *Abuf, cplx_t<T> *Bbuf0, T tol) {
+    using T2 = cplx_t<T>;
+    constexpr bool WANTV = RPLV > 0;
+    constexpr int RPLV1 = WANTV ? RPLV : 1;
+    const int w = s.P, G = s.G, LD = s.ldx, VOFF = s.ldv;
+    const int tid = threadIdx.x, k = tid / G, g = tid % G;
+    const bool active = k < w;
+    constexpr uint32_t T2SZ = sizeof(T2);
+    const uint32_t rstride = (uint32_t)G * T2SZ;
+    const uint32_t voff_b = (uint32_t)VOFF * T2SZ;
+    const uint32_t colb = (uint32_t)LD * T2SZ;
+    T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
+    bool rot = false, bad = false;
+    int *pos = flags + 4;
+    const size_t panel_elems = (size_t)w * LD;
+    int bcur = flags[2];
+    cplx_t<T> *Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
+            // ---- a panel -> registers -------------------------------------
+            T2 ra[RPLX], rav[RPLV1];
+            if (active) {
+                const uint32_t aa = smem_u32(Abuf) + k * colb + g * T2SZ;
+                col_load<T, RPLX>(ra, aa, rstride);
+                if constexpr (WANTV) col_load<T, RPLV1>(rav, aa + voff_b, rstride);
+            }
+
+            // ---- 2C-1 super-rounds of cross pairs ---------------------------
+#pragma unroll 1
+            for (int t = 0; t < 2 * C - 1; ++t) {
+#pragma unroll 1
+                for (int sr = 0; sr < w; ++sr) {
+                    int j = k + sr;
+                    if (j >= w) j -= w;
+                    T2 y[RPLX], yv[RPLV1];
+                    T al = 0, be = 0, gr = 0, gi = 0;
+                    const uint32_t ab = smem_u32(Bbuf) + j * colb + g * T2SZ;
+                    if (active) {
+                        col_load<T, RPLX>(y, ab, rstride);
+#pragma unroll
+                        for (int i = 0; i < RPLX; ++i) {
+                            al += ra[i].x * ra[i].x + ra[i].y * ra[i].y;
+                            be += y[i].x * y[i].x + y[i].y * y[i].y;
+                            gr += ra[i].x * y[i].x + ra[i].y * y[i].y;
+                            gi += ra[i].x * y[i].y - ra[i].y * y[i].x;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        if (off < G) {
+                            al += __shfl_xor_sync(0xffffffffu, al, off);
+                            be += __shfl_xor_sync(0xffffffffu, be, off);
+                            gr += __shfl_xor_sync(0xffffffffu, gr, off);
+                            gi += __shfl_xor_sync(0xffffffffu, gi, off);
+                        }
+                    }
+                    if (active) {
+                        Rot<T> R;
+                        const int act = rot_params<T>(al, be, gr, gi, tol, R);
+                        if (act < 0) {
+                            bad = true;
+                        } else if (act > 0) {
+                            rot = true;
+#pragma unroll
+                            for (int i = 0; i < RPLX; ++i) rot_apply<T>(ra[i], y[i], R);
+                            col_store<T, RPLX>(y, ab, rstride);
+                            if constexpr (WANTV) {  // V rows only after the decision
+                                col_load<T, RPLV1>(yv, ab + voff_b, rstride);
+#pragma unroll
+                                for (int i = 0; i < RPLV; ++i) rot_apply<T>(rav[i], yv[i], R);
+                                col_store<T, RPLV1>(yv, ab + voff_b, rstride);
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+                if constexpr (C > 1) {
+                    if (t == 2 * C - 2) break;
+                    // ---- panel rotation across the cluster --------------------
+                    if (active) {  // a registers -> Abuf (peers may pull it)
+                        const uint32_t aa = smem_u32(Abuf) + k * colb + g * T2SZ;
+                        col_store<T, RPLX>(ra, aa, rstride);
+                        if constexpr (WANTV) col_store<T, RPLV1>(rav, aa + voff_b, rstride);
+                    }
+                    cluster_sync_all();
+                    cg::cluster_group cl = cg::this_cluster();
+                    T2 *Bnext = Bbuf0 + (size_t)(bcur ^ 1) * panel_elems;
+                    // new a: position rank <- rank+1 (CTA rank+1's a; CTA C-1 takes its own b)
+                    if (rank != 0 && active) {
+                        const uint32_t src = (rank == C - 1)
+                                                 ? map_rank(smem_u32(Bbuf), rank)
+                                                 : map_rank(smem_u32(Abuf), rank + 1);
+                        const uint32_t aa = src + k * colb + g * T2SZ;
+                        col_load_cluster<T, RPLX>(ra, aa, rstride);
+                        if constexpr (WANTV) col_load_cluster<T, RPLV1>(rav, aa + voff_b, rstride);
+                    }
+                    // new b: position 2C-1-rank <- 2C-rank (CTA rank-1's b; CTA 0 takes CTA 1's a)
+                    {
+                        const T2 *src;
+                        if (rank == 0) src = cl.map_shared_rank(Abuf, 1);
+                        else src = cl.map_shared_rank(Bbuf0 + (size_t)bcur * panel_elems, rank - 1);
+                        const float4 *s4 = reinterpret_cast<const float4 *>(src);
+                        float4 *d4 = reinterpret_cast<float4 *>(Bnext);
+                        const size_t n4 = panel_elems * sizeof(T2) / sizeof(float4);
+                        for (size_t x = tid; x < n4; x += blockDim.x) d4[x] = s4[x];
+                    }
+                    int np = 0;
+                    if (tid < 2 * C) np = (tid == 0) ? pos[0] : (tid == 2 * C - 1 ? pos[1] : pos[tid + 1]);
+                    cluster_sync_all();
+                    if (tid < 2 * C) pos[tid] = np;
+                    bcur ^= 1;
+                    Bbuf = Bnext;
+                    if (tid == 0) flags[2] = bcur;
+                    __syncthreads();
+                }
+            }
+            // ---- a registers back to shared memory ---------------------------
+            if (active) {
+                const uint32_t aa = smem_u32(Abuf) + k * colb + g * T2SZ;
+                col_store<T, RPLX>(ra, aa, rstride);
+                if constexpr (WANTV) col_store<T, RPLV1>(rav, aa + voff_b, rstride);
+            }
+    return (rot ? 1 : 0) | (bad ? 2 : 0);
+}
+
+template <typename T, int C, int RPLX, int RPLV>
+__global__ void __launch_bounds__(JAC_MAX_THREADS)
+jacobi_panel_kernel(const JacArgs<T> a) {
+    using T2 = cplx_t<T>;
+    constexpr bool WANTV = RPLV > 0;
+    constexpr int RPLV1 = WANTV ? RPLV : 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const JacShape &s = a.s;
+    int rank = 0;
+    if constexpr (C > 1) rank = (int)cg::this_cluster().block_rank();
+    const long long cid = blockIdx.x / C;
+
+    const int w = s.P;            // panel width (pairs per round)
+    const int G = s.G;
+    const int LD = s.ldx;         // column stride (complex) of [X rows | V rows]
+    const int VOFF = s.ldv;       // row offset of the V rows inside a column
+    const int ncp = s.ncp, nc = s.nc, mr = s.mr;
+    const int tid = threadIdx.x, k = tid / G, g = tid % G;
+    const bool active = k < w;
+    const T tol = a.tol;
+
+    T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);            // [ncp] squared norms
+    int *perm = reinterpret_cast<int *>(smem + s.off_perm);       // [2 ncp]
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);      // [4] rot, bad | [64] positions
+    T2 *Abuf = reinterpret_cast<T2 *>(smem + s.off_x);            // [w][LD]
+    T2 *Bbuf0 = reinterpret_cast<T2 *>(smem + s.off_v);           // [w][LD] (x2 when C>1)
+    const size_t panel_elems = (size_t)w * LD;
+    constexpr uint32_t T2SZ = sizeof(T2);
+    const uint32_t rstride = (uint32_t)G * T2SZ;        // bytes between a lane's rows
+    const uint32_t voff_b = (uint32_t)VOFF * T2SZ;       // byte offset of the V rows
+    const uint32_t colb = (uint32_t)LD * T2SZ;           // bytes per column
+
+    // panel ids by position (identical bookkeeping in every CTA) live in shared
+    // memory: [0,32) current positions, [32,64) positions at sweep start
+    int *pos = flags + 4;
+    int *start_pos = flags + 4 + 32;
+    for (long long f = cid; f < a.count; f += s.num_clusters) {
+        if (tid < 32) pos[tid] = tid;
+        if (tid == 0) flags[2] = 0;  // current b buffer
+        __syncthreads();
+        int bcur = 0;
+        T2 *Bbuf = Bbuf0;
+
+        // ---- load the two initial panels (a = panel rank, b = panel 2C-1-rank)
+        const long long mid = a.index ? a.index[f] : f;  // matrix id (outputs too)
+        {
+            const T2 *A = a.blocks + (size_t)mid * a.co * a.ci;
+            const T2 *X0 = a.initX ? a.initX + (size_t)f * mr * nc : nullptr;
+            const T2 *V0 = a.initV ? a.initV + (size_t)a.initV_index[f] * nc * nc : nullptr;
+            for (int half = 0; half < 2; ++half) {
+                const int panel = half == 0 ? rank : 2 * C - 1 - rank;
+                T2 *dst = half == 0 ? Abuf : Bbuf;
+                const int c0 = panel * w;
+                const int rows_x = G * RPLX;
+                for (int idx = tid; idx < w * rows_x; idx += blockDim.x) {
+                    int jj, r;
+                    if (!s.wide || X0) { r = idx / w; jj = idx - r * w; }
+                    else { jj = idx / rows_x; r = idx - jj * rows_x; }
+                    const int j = c0 + jj;
+                    T2 v = mk<T>(0, 0);
+                    if (r < mr && j < nc) {
+                        if (X0) v = X0[(size_t)r * nc + j];
+                        else if (!s.wide) v = A[(size_t)r * a.ci + j];
+                        else { v = A[(size_t)j * a.ci + r]; v.y = -v.y; }
+                    }
+                    dst[(size_t)jj * LD + r] = v;
+                }
+                if constexpr (WANTV) {
+                    const int rows_v = G * RPLV;
+                    for (int idx = tid; idx < w * rows_v; idx += blockDim.x) {
+                        int jj, r;
+                        if (V0) { r = idx / w; jj = idx - r * w; }
+                        else { jj = idx / rows_v; r = idx - jj * rows_v; }
+                        const int j = c0 + jj;
+                        T2 v = mk<T>((r == j && r < nc) ? (T)1 : (T)0, 0);
+                        if (V0) v = (r < nc && j < nc) ? V0[(size_t)r * nc + j] : mk<T>(0, 0);
+                        dst[(size_t)jj * LD + VOFF + r] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        int info = -1;
+        for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+            const int start_a = pos[rank];              // panel ids at the start of the sweep
+            const int start_b = pos[2 * C - 1 - rank];
+            __syncthreads();
+            if (tid < 32) start_pos[tid] = pos[tid];
+
+            int fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
+            fl |= panel_cross<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+            bcur = flags[2];
+            Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
+            const bool rot = fl & 1, bad = fl & 2;
+            // ---- sweep verdict, OR-ed over the cluster ------------------------
+            int any_bad = __syncthreads_or(bad);
+            int any_rot = __syncthreads_or(rot);
+            if constexpr (C > 1) {
+                if (tid == 0) {
+                    flags[0] = any_rot;
+                    flags[1] = any_bad;
+                }
+                cluster_sync_all();
+                cg::cluster_group cl = cg::this_cluster();
+                for (int d = 0; d < C; ++d) {
+                    const int *pf = cl.map_shared_rank(flags, d);
+                    any_rot |= pf[0];
+                    any_bad |= pf[1];
+                }
+                cluster_sync_all();
+            }
+            if (any_bad) break;
+            if (!any_rot) {
+                info = sweep + 1;
+                break;
+            }
+        }
+
+        // ---- epilogue ---------------------------------------------------------
+        // squared norms were recorded per column at round 0 of the last sweep
+        // by the CTA that held the column then; gather them from their owners
+        if constexpr (C > 1) {
+            T *stage = reinterpret_cast<T *>(smem + s.off_send);  // [ncp]
+            cluster_sync_all();
+            cg::cluster_group cl = cg::this_cluster();
+            for (int j = tid; j < ncp; j += blockDim.x) {
+                const int panel = j / w;
+                int p0 = 0;
+                for (int p = 0; p < 2 * C; ++p)
+                    if (start_pos[p] == panel) p0 = p;
+                const int owner = pos_owner(p0, C);
+                stage[j] = (owner == rank) ? sig2[j] : cl.map_shared_rank(sig2, owner)[j];
+            }
+            cluster_sync_all();  // every CTA has read its peers' sig2
+            for (int j = tid; j < ncp; j += blockDim.x) sig2[j] = stage[j];
+            __syncthreads();
+        }
+        for (int j = tid; j < ncp; j += blockDim.x) {
+            sig2[j] = epi_sqrt(sig2[j]);
+            perm[j] = j;
+        }
+        __syncthreads();
+        if (info >= 0) {
+            int *rnk = perm + ncp;
+            for (int j = tid; j < nc; j += blockDim.x) {
+                const T sj = sig2[j];
+                int pp = 0;
+                for (int i = 0; i < nc; ++i) {
+                    const T si = sig2[i];
+                    pp += (si > sj) || (si == sj && i < j);
+                }
+                rnk[j] = pp;
+            }
+            __syncthreads();
+            for (int j = tid; j < nc; j += blockDim.x) perm[rnk[j]] = j;
+            __syncthreads();
+        }
+        if (rank == 0) {
+            for (int p = tid; p < nc; p += blockDim.x) a.sigma[(size_t)mid * nc + p] = sig2[perm[p]];
+            if (tid == 0) a.info[mid] = info;
+        }
+        if constexpr (WANTV) {
+            // inverse permutation: column j -> output position
+            int *ipos = perm + ncp;
+            __syncthreads();
+            for (int p = tid; p < nc; p += blockDim.x) ipos[perm[p]] = p;
+            __syncthreads();
+            const int pa = pos[rank], pb = pos[2 * C - 1 - rank];
+            for (int half = 0; half < 2; ++half) {
+                const T2 *src = half == 0 ? Abuf : Bbuf;
+                const int c0 = (half == 0 ? pa : pb) * w;
+                if (a.Uw) {
+                    for (int idx = tid; idx < mr * w; idx += blockDim.x) {
+                        const int r = idx / w, jj = idx - r * w, j = c0 + jj;
+                        if (j >= nc) continue;
+                        const T sj = sig2[j];
+                        const T den = sj > (T)0 ? sj : (T)1;
+                        const T2 v = src[(size_t)jj * LD + r];
+                        a.Uw[((size_t)mid * mr + r) * nc + ipos[j]] = mk<T>(epi_div(v.x, den), epi_div(v.y, den));
+                    }
+                }
+                if (a.Vw) {
+                    for (int idx = tid; idx < nc * w; idx += blockDim.x) {
+                        const int r = idx / w, jj = idx - r * w, j = c0 + jj;
+                        if (j >= nc) continue;
+                        a.Vw[((size_t)mid * nc + r) * nc + ipos[j]] = src[(size_t)jj * LD + VOFF + r];
+                    }
+                }
+            }
+            if (a.zero_sigma && rank == 0 && tid == 0) {
+                int z = 0;
+                for (int j = 0; j < nc; ++j) z |= !(sig2[j] > (T)0);
+                a.zero_sigma[mid] = z;
+            }
+        }
+        if constexpr (C > 1) cluster_sync_all();  // peers done reading this CTA's buffers
+        __syncthreads();
+    }
+}
+
+}  // namespace cs

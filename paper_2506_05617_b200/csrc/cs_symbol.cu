@@ -22,7 +22,7 @@
 namespace cs {
 
 constexpr int K1_THREADS = 256;
-constexpr int K1_JC = 16;       // grid columns j per CTA
+constexpr int K1_JC = 64;       // grid columns j per CTA (W and G_p reused across them)
 constexpr int K1_KHMAX = 8;     // separable path handles k_h <= 8
 
 __device__ __forceinline__ long long imod(long long a, long long n) {

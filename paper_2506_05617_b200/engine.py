@@ -276,6 +276,115 @@ def batched_svd_grouped(groups, dtype: str, want_vectors: bool, tol=DEFAULT_SVD_
     return outs
 
 
+def plan_kind(count: int, co: int, ci: int, dtype: str, want_vectors: bool) -> int:
+    return int(_lib.load().cs_batched_svd_plan_kind(dtype_code(dtype), count, co, ci,
+                                                    int(want_vectors)))
+
+
+def batched_svd_indexed(blocks, dtype: str, want_vectors: bool, index, out: SvdBatch,
+                        tol=DEFAULT_SVD_TOL, max_sweeps=DEFAULT_MAX_SWEEPS, init_X=None,
+                        init_V=None, init_V_index=None):
+    """Solve blocks[index[i]] (outputs at index[i]); optional warm start from
+    init_X[i] / init_V[init_V_index[i]] (cs_batched_svd_indexed)."""
+    _, co, ci = blocks.shape
+    count = index.shape[0]
+    dev = blocks.device
+    lib = _lib.load()
+    code = dtype_code(dtype)
+    ws_bytes = lib.cs_batched_svd_workspace(code, count, co, ci, int(want_vectors))
+    ws = WORKSPACE.get(dev, ws_bytes)
+    etol = effective_tol(tol, dtype, max(co, ci))
+    st = lib.cs_batched_svd_indexed(ptr(blocks), code, count, co, ci, int(want_vectors), etol,
+                                    int(max_sweeps), ptr(index), ptr(init_X), ptr(init_V),
+                                    ptr(init_V_index), ptr(out.sigma), ptr(out.U), ptr(out.V),
+                                    ptr(out.info), ptr(out.zero), ptr(ws), ws_bytes,
+                                    stream_ptr(dev))
+    _lib.check(st, "cs_batched_svd_indexed")
+    return out
+
+
+def warm_start_gemm(blocks, dtype: str, warm_ids, seed_ids, Vw, out_X):
+    _, co, ci = blocks.shape
+    st = _lib.load().cs_warm_start_gemm(ptr(blocks), dtype_code(dtype), co, ci,
+                                        warm_ids.shape[0], ptr(warm_ids), ptr(seed_ids),
+                                        ptr(Vw), ptr(out_X), stream_ptr(blocks.device))
+    _lib.check(st, "cs_warm_start_gemm")
+    return out_X
+
+
+_WARM_PLANS = {}
+
+
+def warm_plan(n: int, m: int, u0: int, count: int, device):
+    """Seeds / warm-started blocks over representatives [u0, u0+count).
+
+    Within each grid row, consecutive representatives are frequency
+    neighbours (j, j+1): triples are solved as [warm, seed, warm] with the
+    middle one cold; a trailing pair is [seed, warm], a single one a seed.
+    Returns device int64 tensors (seeds, warm, seed_of_warm), local indices."""
+    key = (n, m, u0, count, str(device))
+    if key in _WARM_PLANS:
+        return _WARM_PLANS[key]
+    reps = half_grid_indices(n, m)[u0:u0 + count]
+    rows = reps // m
+    seeds, warm, seed_of = [], [], []
+    a = 0
+    while a < count:
+        b = a
+        while b < count and rows[b] == rows[a]:
+            b += 1
+        for p in range(a, b, 3):
+            grp = list(range(p, min(p + 3, b)))
+            if len(grp) == 3:
+                seeds.append(grp[1])
+                warm += [grp[0], grp[2]]
+                seed_of += [grp[1], grp[1]]
+            elif len(grp) == 2:
+                seeds.append(grp[0])
+                warm.append(grp[1])
+                seed_of.append(grp[0])
+            else:
+                seeds.append(grp[0])
+        a = b
+    t = lambda x: torch.tensor(np.asarray(x, dtype=np.int64), device=device)
+    plan = (t(seeds), t(warm), t(seed_of))
+    _WARM_PLANS[key] = plan
+    return plan
+
+
+def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SVD_TOL,
+                     max_sweeps=DEFAULT_MAX_SWEEPS, values_out: SvdBatch | None = None):
+    """All blocks of a representative range, neighbours warm-started from
+    their seed's right factor (cs_warm_start_gemm + cs_batched_svd_indexed)."""
+    count, co, ci = blocks.shape
+    dev = blocks.device
+    out = values_out or alloc_svd_outputs(count, co, ci, dtype, True, dev)
+    seeds, warm, seed_of = warm_plan(n, m, u0, count, dev)
+    batched_svd_indexed(blocks, dtype, True, seeds, out, tol, max_sweeps)
+    if warm.shape[0]:
+        wide = co < ci
+        mr, nc = (ci, co) if wide else (co, ci)
+        Vw = out.U if wide else out.V
+        Xw = torch.empty((warm.shape[0], mr, nc), dtype=blocks.dtype, device=dev)
+        warm_start_gemm(blocks, dtype, warm, seed_of, Vw, Xw)
+        batched_svd_indexed(blocks, dtype, True, warm, out, tol, max_sweeps, init_X=Xw,
+                            init_V=Vw, init_V_index=seed_of)
+        del Xw
+    complete_zero_columns(out, co, ci, dtype)
+    return out
+
+
+def use_warm_start(count: int, co: int, ci: int, dtype: str, want_vectors: bool,
+                   requested=None) -> bool:
+    """Warm start pays off when vectors are computed anyway (seeds need V)."""
+    env = os.environ.get("CS_WARM_START")
+    if requested is None:
+        requested = (env != "0") if env is not None else want_vectors
+    if not requested or count < 3:
+        return False
+    return plan_kind(count, co, ci, dtype, True) == 2
+
+
 def complete_zero_columns(out: SvdBatch, co: int, ci: int, dtype: str):
     """blocksvd.py:184-198 on the factor of the working (tall) matrix."""
     if out.zero is None or out.sigma.shape[0] == 0:

@@ -44,8 +44,13 @@ class DeviceSpectrum:
 def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
                tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
                u0: int = 0, count: int | None = None, assemble: bool = True,
-               timer: engine.Timer | None = None, field_out=None) -> DeviceSpectrum:
-    """K1 -> K2/K3 -> assembly on the current stream, no host synchronisation."""
+               timer: engine.Timer | None = None, field_out=None,
+               warm_start=None) -> DeviceSpectrum:
+    """K1 -> K2/K3 -> assembly on the current stream, no host synchronisation.
+
+    ``warm_start`` (default: when vectors are requested and the panel kernel
+    applies) solves frequency triples [warm, seed, warm]: the seed cold, its
+    two grid neighbours from X A V_seed, which needs ~half the sweeps."""
     total = engine.half_grid_count(n, m)
     if count is None:
         count = total - u0
@@ -55,7 +60,13 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
                               out=field_out)
     if timer:
         timer.mark("t1")
-    out = engine.batched_svd(fld, dtype, want_vectors, tol, max_sweeps)
+    co, ci = w_dev.shape[0], w_dev.shape[1]
+    if engine.use_warm_start(count, co, ci, dtype, want_vectors, warm_start):
+        out = engine.batched_svd_warm(fld, dtype, n, m, u0, tol, max_sweeps)
+        if not want_vectors:
+            out.U = out.V = None
+    else:
+        out = engine.batched_svd(fld, dtype, want_vectors, tol, max_sweeps)
     if timer:
         timer.mark("t2")
     values = None
