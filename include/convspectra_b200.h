@@ -122,14 +122,16 @@ int cs_warm_start_gemm(const void *blocks, int dtype, int c_out, int c_in, long 
                        void *out_X, void *stream);
 
 /* Heterogeneous batch in one call (cfg4: 16 layers, 4 shapes).  `groups` is a
- * HOST array; each group is solved like cs_batched_svd; groups run
- * concurrently on forked streams joined back into `stream`. */
+ * HOST array; each group is solved like cs_batched_svd (with its own tol when
+ * group.tol > 0, else the call's); groups run concurrently on forked streams
+ * joined back into `stream`. */
 typedef struct cs_svd_group {
     const void *blocks;
     long long count;
     int c_out, c_in;
     void *sigma, *U, *V;
     int *info, *zero_sigma;
+    double tol;
 } cs_svd_group;
 size_t cs_batched_svd_grouped_workspace(const cs_svd_group *groups, int num_groups,
                                         int dtype, int want_vectors);

@@ -32,7 +32,8 @@ _sz = ctypes.c_size_t
 
 class SvdGroup(ctypes.Structure):
     _fields_ = [("blocks", _vp), ("count", _ll), ("c_out", _i), ("c_in", _i),
-                ("sigma", _vp), ("U", _vp), ("V", _vp), ("info", _vp), ("zero_sigma", _vp)]
+                ("sigma", _vp), ("U", _vp), ("V", _vp), ("info", _vp), ("zero_sigma", _vp),
+                ("tol", _d)]
 
 
 _SIGNATURES = {

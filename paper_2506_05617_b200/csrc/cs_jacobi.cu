@@ -366,7 +366,8 @@ extern "C" int cs_batched_svd_grouped(const cs_svd_group *groups, int num_groups
     cudaStream_t st = (cudaStream_t)stream;
     if (num_groups == 1)
         return cs_batched_svd(groups[0].blocks, dtype, groups[0].count, groups[0].c_out,
-                              groups[0].c_in, want_vectors, tol, max_sweeps, groups[0].sigma,
+                              groups[0].c_in, want_vectors, groups[0].tol > 0 ? groups[0].tol : tol,
+                              max_sweeps, groups[0].sigma,
                               groups[0].U, groups[0].V, groups[0].info, groups[0].zero_sigma,
                               workspace, workspace_bytes, stream);
     // fork: every group on its own stream so small and large shapes share the SMs
@@ -391,8 +392,8 @@ extern "C" int cs_batched_svd_grouped(const cs_svd_group *groups, int num_groups
             status = fail(CS_ENOMEM, "grouped SVD: workspace too small");
             break;
         }
-        status = cs_batched_svd(G.blocks, dtype, G.count, G.c_out, G.c_in, want_vectors, tol,
-                                max_sweeps, G.sigma, G.U, G.V, G.info, G.zero_sigma,
+        status = cs_batched_svd(G.blocks, dtype, G.count, G.c_out, G.c_in, want_vectors,
+                                G.tol > 0 ? G.tol : tol, max_sweeps, G.sigma, G.U, G.V, G.info, G.zero_sigma,
                                 need ? (char *)workspace + off : nullptr, need, sides[g % nside]);
         off += (need + 255) & ~(size_t)255;
     }

@@ -260,13 +260,12 @@ def batched_svd_grouped(groups, dtype: str, want_vectors: bool, tol=DEFAULT_SVD_
         o = alloc_svd_outputs(count, co, ci, dtype, want_vectors, dev)
         outs.append(o)
         table[g] = _lib.SvdGroup(ptr(blk), count, co, ci, ptr(o.sigma), ptr(o.U), ptr(o.V),
-                                 ptr(o.info), ptr(o.zero))
+                                 ptr(o.info), ptr(o.zero), effective_tol(tol, dtype, max(co, ci)))
         rows = max(rows, co, ci)
     code = dtype_code(dtype)
     ws_bytes = lib.cs_batched_svd_grouped_workspace(table, len(groups), code, int(want_vectors))
     ws = WORKSPACE.get(dev, ws_bytes)
-    # one tol for the call: floor of the largest block (conservative for fp32)
-    etol = effective_tol(tol, dtype, rows)
+    etol = effective_tol(tol, dtype, rows)  # per-group tols override it
     st = lib.cs_batched_svd_grouped(table, len(groups), code, int(want_vectors), etol,
                                     int(max_sweeps), ptr(ws), ws_bytes, stream_ptr(dev))
     _lib.check(st, "cs_batched_svd_grouped")
@@ -313,63 +312,82 @@ def warm_start_gemm(blocks, dtype: str, warm_ids, seed_ids, Vw, out_X):
 
 
 _WARM_PLANS = {}
+WARM_DEPTH = int(os.environ.get("CS_WARM_DEPTH", "3"))
 
 
-def warm_plan(n: int, m: int, u0: int, count: int, device):
-    """Seeds / warm-started blocks over representatives [u0, u0+count).
+def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = None):
+    """Stages of a warm-started solve over representatives [u0, u0+count).
 
-    Within each grid row, consecutive representatives are frequency
-    neighbours (j, j+1): triples are solved as [warm, seed, warm] with the
-    middle one cold; a trailing pair is [seed, warm], a single one a seed.
-    Returns device int64 tensors (seeds, warm, seed_of_warm), local indices."""
-    key = (n, m, u0, count, str(device))
+    Representatives are nodes of the frequency lattice (i, j); two are
+    neighbours when they differ by one grid step in i or j (their symbols
+    differ by O(2 pi/n) relative).  Cold seeds sit on a (2*depth+1)-periodic
+    lattice; a breadth-first search from the seeds assigns every other
+    representative to the stage equal to its lattice distance, warm-started
+    from its BFS parent (solved one stage earlier).  Representatives not
+    reachable within the range become seeds.  Returns [(ids, pred_or_None)]
+    per stage as device int64 tensors of local indices."""
+    depth = WARM_DEPTH if depth is None else depth
+    key = (n, m, u0, count, str(device), depth)
     if key in _WARM_PLANS:
         return _WARM_PLANS[key]
     reps = half_grid_indices(n, m)[u0:u0 + count]
-    rows = reps // m
-    seeds, warm, seed_of = [], [], []
-    a = 0
-    while a < count:
-        b = a
-        while b < count and rows[b] == rows[a]:
-            b += 1
-        for p in range(a, b, 3):
-            grp = list(range(p, min(p + 3, b)))
-            if len(grp) == 3:
-                seeds.append(grp[1])
-                warm += [grp[0], grp[2]]
-                seed_of += [grp[1], grp[1]]
-            elif len(grp) == 2:
-                seeds.append(grp[0])
-                warm.append(grp[1])
-                seed_of.append(grp[0])
-            else:
-                seeds.append(grp[0])
-        a = b
+    ii, jj = reps // m, reps % m
+    local = {(int(a), int(b)): q for q, (a, b) in enumerate(zip(ii, jj))}
+    span = 2 * depth + 1
+    level = np.full(count, -1, dtype=np.int64)
+    parent = np.full(count, -1, dtype=np.int64)
+    frontier = [q for q in range(count) if ii[q] % span == depth % span and jj[q] % span == depth]
+    if not frontier:
+        frontier = [0]
+    for q in frontier:
+        level[q] = 0
+    while True:
+        while frontier:
+            nxt = []
+            for q in frontier:
+                a, b = int(ii[q]), int(jj[q])
+                for nb in ((a, b - 1), (a, b + 1), (a - 1, b), (a + 1, b)):
+                    r = local.get(nb)
+                    if r is not None and level[r] < 0:
+                        level[r] = level[q] + 1
+                        parent[r] = q
+                        nxt.append(r)
+            frontier = nxt
+        left = np.nonzero(level < 0)[0]
+        if len(left) == 0:
+            break
+        level[left[0]] = 0
+        frontier = [int(left[0])]
     t = lambda x: torch.tensor(np.asarray(x, dtype=np.int64), device=device)
-    plan = (t(seeds), t(warm), t(seed_of))
+    plan = []
+    for d in range(int(level.max()) + 1):
+        ids = np.nonzero(level == d)[0]
+        if len(ids):
+            plan.append((t(ids), t(parent[ids]) if d else None))
     _WARM_PLANS[key] = plan
     return plan
 
 
 def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SVD_TOL,
-                     max_sweeps=DEFAULT_MAX_SWEEPS, values_out: SvdBatch | None = None):
-    """All blocks of a representative range, neighbours warm-started from
-    their seed's right factor (cs_warm_start_gemm + cs_batched_svd_indexed)."""
+                     max_sweeps=DEFAULT_MAX_SWEEPS, depth: int | None = None):
+    """All blocks of a representative range; every non-seed block is
+    warm-started from its solved neighbour's right factor
+    (cs_warm_start_gemm + cs_batched_svd_indexed), stage by stage."""
     count, co, ci = blocks.shape
     dev = blocks.device
-    out = values_out or alloc_svd_outputs(count, co, ci, dtype, True, dev)
-    seeds, warm, seed_of = warm_plan(n, m, u0, count, dev)
-    batched_svd_indexed(blocks, dtype, True, seeds, out, tol, max_sweeps)
-    if warm.shape[0]:
-        wide = co < ci
-        mr, nc = (ci, co) if wide else (co, ci)
-        Vw = out.U if wide else out.V
-        Xw = torch.empty((warm.shape[0], mr, nc), dtype=blocks.dtype, device=dev)
-        warm_start_gemm(blocks, dtype, warm, seed_of, Vw, Xw)
-        batched_svd_indexed(blocks, dtype, True, warm, out, tol, max_sweeps, init_X=Xw,
-                            init_V=Vw, init_V_index=seed_of)
-        del Xw
+    out = alloc_svd_outputs(count, co, ci, dtype, True, dev)
+    wide = co < ci
+    mr, nc = (ci, co) if wide else (co, ci)
+    Vw = out.U if wide else out.V
+    for ids, pred in warm_plan(n, m, u0, count, dev, depth):
+        if pred is None:
+            batched_svd_indexed(blocks, dtype, True, ids, out, tol, max_sweeps)
+        else:
+            Xw = torch.empty((ids.shape[0], mr, nc), dtype=blocks.dtype, device=dev)
+            warm_start_gemm(blocks, dtype, ids, pred, Vw, Xw)
+            batched_svd_indexed(blocks, dtype, True, ids, out, tol, max_sweeps, init_X=Xw,
+                                init_V=Vw, init_V_index=pred)
+            del Xw
     complete_zero_columns(out, co, ci, dtype)
     return out
 
