@@ -384,10 +384,10 @@ jacobi_fast_kernel(const JacArgs<T> a) {
                     }
 #pragma unroll
                     for (int i = 0; i < RPL; ++i) {
-                        al += x[i].x * x[i].x + x[i].y * x[i].y;
-                        be += y[i].x * y[i].x + y[i].y * y[i].y;
-                        gr += x[i].x * y[i].x + x[i].y * y[i].y;
-                        gi += x[i].x * y[i].y - x[i].y * y[i].x;
+                        al = fma(x[i].y, x[i].y, fma(x[i].x, x[i].x, al));
+                        be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                        gr = fma(x[i].y, y[i].y, fma(x[i].x, y[i].x, gr));
+                        gi = fma(-x[i].y, y[i].x, fma(x[i].x, y[i].y, gi));
                     }
                 }
 #pragma unroll
@@ -535,10 +535,10 @@ jacobi_generic_kernel(const JacArgs<T> a) {
                         const T2 *xp = Xs + (size_t)p * ldx, *xq = Xs + (size_t)q * ldx;
                         for (int lr = lane_g; lr < R; lr += G) {
                             const T2 x = xp[lr], y = xq[lr];
-                            al += x.x * x.x + x.y * x.y;
-                            be += y.x * y.x + y.y * y.y;
-                            gr += x.x * y.x + x.y * y.y;
-                            gi += x.x * y.y - x.y * y.x;
+                            al = fma(x.y, x.y, fma(x.x, x.x, al));
+                            be = fma(y.y, y.y, fma(y.x, y.x, be));
+                            gr = fma(x.y, y.y, fma(x.x, y.x, gr));
+                            gi = fma(-x.y, y.x, fma(x.x, y.y, gi));
                         }
                     }
 #pragma unroll

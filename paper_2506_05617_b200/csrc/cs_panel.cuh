@@ -137,10 +137,10 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
                         col_load<T, RPLX>(y, aq, rstride);
 #pragma unroll
                         for (int i = 0; i < RPLX; ++i) {
-                            al += x[i].x * x[i].x + x[i].y * x[i].y;
-                            be += y[i].x * y[i].x + y[i].y * y[i].y;
-                            gr += x[i].x * y[i].x + x[i].y * y[i].y;
-                            gi += x[i].x * y[i].y - x[i].y * y[i].x;
+                            al = fma(x[i].y, x[i].y, fma(x[i].x, x[i].x, al));
+                            be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                            gr = fma(x[i].y, y[i].y, fma(x[i].x, y[i].x, gr));
+                            gi = fma(-x[i].y, y[i].x, fma(x[i].x, y[i].y, gi));
                         }
                     }
 #pragma unroll
@@ -232,10 +232,10 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                         col_load<T, RPLX>(y, ab, rstride);
 #pragma unroll
                         for (int i = 0; i < RPLX; ++i) {
-                            al += ra[i].x * ra[i].x + ra[i].y * ra[i].y;
-                            be += y[i].x * y[i].x + y[i].y * y[i].y;
-                            gr += ra[i].x * y[i].x + ra[i].y * y[i].y;
-                            gi += ra[i].x * y[i].y - ra[i].y * y[i].x;
+                            al = fma(ra[i].y, ra[i].y, fma(ra[i].x, ra[i].x, al));
+                            be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                            gr = fma(ra[i].y, y[i].y, fma(ra[i].x, y[i].x, gr));
+                            gi = fma(-ra[i].y, y[i].x, fma(ra[i].x, y[i].y, gi));
                         }
                     }
 #pragma unroll
