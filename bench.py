@@ -262,6 +262,10 @@ def run_ours(args, wl, rank, world, local_rank):
     peaks = read_peaks()
 
     def step(timers=None):
+        if len(layers) > 1 and world == 1:  # cfg4: every layer in one batched call
+            tm = timers[0] if timers else None
+            return cs.lfa_device_multi([(w, l.n, l.m) for l, w in zip(layers, w_dev)], dt,
+                                       wl.vectors, timer=tm)
         outs = []
         for i, (l, w) in enumerate(zip(layers, w_dev)):
             tm = timers[i] if timers else None
@@ -291,6 +295,8 @@ def run_ours(args, wl, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     timers = [[engine.Timer(dev) for _ in layers] for _ in range(args.steps)]
+    if len(layers) > 1 and world == 1:
+        timers = [[engine.Timer(dev)] for _ in range(args.steps)]
     ev[0].record(stream)
     for s in range(args.steps):
         outs = step(timers[s] if world == 1 else None)
@@ -311,9 +317,9 @@ def run_ours(args, wl, rank, world, local_rank):
     roofline = None
     phases = None
     if world == 1:
-        k1 = [tm.seconds("t0", "t1") for row in timers for tm in row]
-        sv = [tm.seconds("t1", "t2") for row in timers for tm in row]
-        asm = [tm.seconds("t2", "t3") for row in timers for tm in row]
+        k1 = [tm.seconds("t0", "t1") for row in timers for tm in row if "t0" in tm.events]
+        sv = [tm.seconds("t1", "t2") for row in timers for tm in row if "t0" in tm.events]
+        asm = [tm.seconds("t2", "t3") for row in timers for tm in row if "t0" in tm.events]
         nl = len(layers)
         phases = {"assembly_K1_ms": 1e3 * sum(k1) / args.steps,
                   "svd_ms": 1e3 * sum(sv) / args.steps,
@@ -348,6 +354,11 @@ def run_ours(args, wl, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
+            if len(layers) > 1 and world == 1:  # one batched call for all layers
+                res = cs.compute_spectra(kernels, [cs.SpatialDims(l.n, l.m) for l in layers],
+                                         values_only=not wl.vectors, device=dev)
+                d2h += sum(r.values.nbytes for r in res)
+                continue
             for k, l in zip(kernels, layers):
                 dims = cs.SpatialDims(l.n, l.m)
                 if world == 1:
@@ -367,8 +378,10 @@ def run_ours(args, wl, rank, world, local_rank):
         el = float(te.item())
         e2e = {"value": svs * args.e2e_steps / el, "unit": "singular values/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.e2e_steps,
-               "api": "paper_2506_05617_b200.compute_spectrum(kernel, dims, values_only=False)"
-                      if world == 1 else "distributed.lfa_sharded (host weights in, sorted values out)"}
+               "api": ("distributed.lfa_sharded (host weights in, sorted values out)" if world > 1
+                       else "paper_2506_05617_b200.compute_spectra(kernels, dims) (one batched call)"
+                       if len(layers) > 1 else
+                       f"paper_2506_05617_b200.compute_spectrum(kernel, dims, values_only={not wl.vectors})")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -379,7 +392,7 @@ def run_ours(args, wl, rank, world, local_rank):
     # launch when cold) + zero-column completion (vectors); then gather, CUB
     # onesweep radix sort (histogram + exclusive-sum + 4 passes) and widen
     per_step = 0
-    for l in layers:
+    for l in (layers if not (len(layers) > 1 and world == 1) else []):
         total = half_count(l.n, l.m)
         u0, cnt = (0, total) if world == 1 else shard_range(total, rank, world)
         if engine.use_warm_start(cnt, l.c_out, l.c_in, dt, wl.vectors):
@@ -387,7 +400,10 @@ def run_ours(args, wl, rank, world, local_rank):
             per_step += 1 + stages + (stages - 1) + 1
         else:
             per_step += 1 + 1 + (1 if wl.vectors else 0)
-    per_step += 1 + 6 + 1
+    if len(layers) > 1 and world == 1:  # K1 + one Jacobi launch per layer, then per-layer sort
+        per_step = len(layers) * (1 + 1 + (1 if wl.vectors else 0) + 1 + 6 + 1)
+    else:
+        per_step += 1 + 6 + 1
     launches = args.steps * per_step
 
     if rank == 0:

@@ -11,6 +11,7 @@
 // CTA, 256x128 on 2, 256x256 + V on 8); a generic kernel that re-reads rows
 // (shared or global memory) keeps every other size correct.
 #include <algorithm>
+#include <cstdlib>
 
 #include "cs_jacobi.cuh"
 #include "cs_panel.cuh"
@@ -119,10 +120,14 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     const int rplx = std::max(2, pow2ceil((s.mr + G - 1) / G));
     const int rplv = wantv ? rplx : 0;
     const int budget = sizeof(T) == 4 ? 16 : 8;  // complex rows per column held in registers
-    if (rplx + rplv > budget) return false;
+    // with vectors, X and V rows go to separate warps when 2x the threads fit
+    // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
+    s.split = (wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&
+               rplx <= budget / 2 && std::getenv("CS_NO_SPLIT") == nullptr) ? 1 : 0;
+    if (!s.split && rplx + rplv > budget) return false;
     s.G = G;
     s.RPL = rplx;
-    s.threads = ((w * G + 31) / 32) * 32;
+    s.threads = s.split ? 2 * w * G : ((w * G + 31) / 32) * 32;
     const int T2sz = 2 * sizeof(T);
     s.ldv = G * rplx;  // row offset of the V rows in a column
     s.ldx = pad_ld(G * (rplx + rplv), G, T2sz);
@@ -133,7 +138,9 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     off = align16(off + 2 * s.ncp * sizeof(int));
     s.off_send = off;  // staging for the cluster norm gather
     off = align16(off + s.ncp * sizeof(T));
-    s.off_recv = s.off_mbar = off;  // sweep flags + panel position tables
+    s.off_recv = off;  // split mode: rotation parameters [2][w]
+    off = align16(off + 2 * (size_t)w * 4 * sizeof(T) + 64);
+    s.off_mbar = off;  // sweep flags + panel position tables
     off = align16(off + (4 + 64) * sizeof(int));
     s.off_x = off;
     const size_t panel = (size_t)w * s.ldx * T2sz;

@@ -43,6 +43,7 @@ struct JacShape {
     int mr, nc, ncp, P, R, Rv, ldx, ldv, G, RPL, wide, C, threads, nbuf;
     size_t off_sig, off_perm, off_send, off_recv, off_mbar, off_x, off_v, smem;
     int smem_resident;
+    int split;  // panel kernel: separate X and V warps (2x threads)
     long long num_clusters;
     size_t scratch_per_cta;  // complex elements, generic global-memory mode
 };

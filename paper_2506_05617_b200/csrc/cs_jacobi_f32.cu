@@ -28,10 +28,13 @@ static int fast_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry
 
 template <int C_, int RPL_>
 static int panel_rpl(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
+    if constexpr (2 * RPL_ <= 16 && true)
+        if (wantv && a.s.split)
+            return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_, true>, a, st, dry, ncl);
     if constexpr (2 * RPL_ <= 16)
-        if (wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_>, a, st, dry, ncl);
+        if (wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_, false>, a, st, dry, ncl);
     if constexpr (RPL_ <= 16)
-        if (!wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, 0>, a, st, dry, ncl);
+        if (!wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, 0, false>, a, st, dry, ncl);
     return fail(CS_EINVAL, "batched SVD: panel rows per lane exceed the register budget");
 }
 

@@ -28,10 +28,13 @@ static int fast_c(const JacArgs<double> &a, bool wantv, cudaStream_t st, bool dr
 
 template <int C_, int RPL_>
 static int panel_rpl(const JacArgs<double> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
+    if constexpr (2 * RPL_ <= 8 && false)
+        if (wantv && a.s.split)
+            return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, RPL_, true>, a, st, dry, ncl);
     if constexpr (2 * RPL_ <= 8)
-        if (wantv) return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, RPL_>, a, st, dry, ncl);
+        if (wantv) return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, RPL_, false>, a, st, dry, ncl);
     if constexpr (RPL_ <= 8)
-        if (!wantv) return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, 0>, a, st, dry, ncl);
+        if (!wantv) return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, 0, false>, a, st, dry, ncl);
     return fail(CS_EINVAL, "batched SVD: panel rows per lane exceed the register budget");
 }
 

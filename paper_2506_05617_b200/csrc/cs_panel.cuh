@@ -316,8 +316,250 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
     return (rot ? 1 : 0) | (bad ? 2 : 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// Split-role variant (vectors requested): threads [0, wG) are X warps, threads
+// [wG, 2wG) V warps.  X warps reduce and rotate the X rows and publish the
+// rotation of every pair slot (prm, double-buffered by round parity); V warps
+// apply the same rotation to the V rows ONE ROUND LATER.  V rows never enter
+// a reduction, so this is exact reordering: twice the warps per SM with half
+// the live registers each, and the V FMA work fills the X warps' shuffle /
+// parameter latency.  Every phase runs one extra "drain" iteration.
+// ---------------------------------------------------------------------------
+template <typename T> struct __align__(16) Prm { T cm1, wr, wi; int act; };
+
 template <typename T, int C, int RPLX, int RPLV>
-__global__ void __launch_bounds__(JAC_MAX_THREADS)
+__device__ __noinline__ int panel_within_split(const JacShape &s, unsigned char *smem,
+                                               cplx_t<T> *Abuf, cplx_t<T> *Bbuf, int start_a,
+                                               int start_b, T tol) {
+    using T2 = cplx_t<T>;
+    const int w = s.P, G = s.G, LD = s.ldx, VOFF = s.ldv;
+    const bool xrole = (int)threadIdx.x < w * G;
+    const int ltid = xrole ? threadIdx.x : threadIdx.x - w * G;
+    const int k = ltid / G, g = ltid % G;
+    const bool active = k < w;
+    constexpr uint32_t T2SZ = sizeof(T2);
+    const uint32_t rstride = (uint32_t)G * T2SZ;
+    const uint32_t voff_b = (uint32_t)VOFF * T2SZ;
+    const uint32_t colb = (uint32_t)LD * T2SZ;
+    T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
+    Prm<T> *prm = reinterpret_cast<Prm<T> *>(smem + s.off_recv);  // [2][w]
+    bool rot = false, bad = false;
+    const int hw = w / 2;
+    const int kk = k % hw;
+    T2 *panel = (k < hw) ? Abuf : Bbuf;
+    const int pid = (k < hw) ? start_a : start_b;
+#pragma unroll 1
+    for (int r = 0; r < w; ++r) {  // w-1 rounds + 1 drain
+        if (xrole) {
+            T al = 0, be = 0, gr = 0, gi = 0;
+            int p = 0, q = 0;
+            T2 x[RPLX], y[RPLX];
+            const bool live = active && r < w - 1;
+            if (live) {
+                pair_cols(kk, r, w, p, q);
+                col_load<T, RPLX>(x, smem_u32(panel) + p * colb + g * T2SZ, rstride);
+                col_load<T, RPLX>(y, smem_u32(panel) + q * colb + g * T2SZ, rstride);
+#pragma unroll
+                for (int i = 0; i < RPLX; ++i) {
+                    al = fma(x[i].y, x[i].y, fma(x[i].x, x[i].x, al));
+                    be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                    gr = fma(x[i].y, y[i].y, fma(x[i].x, y[i].x, gr));
+                    gi = fma(-x[i].y, y[i].x, fma(x[i].x, y[i].y, gi));
+                }
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                if (off < G) {
+                    al += __shfl_xor_sync(0xffffffffu, al, off);
+                    be += __shfl_xor_sync(0xffffffffu, be, off);
+                    gr += __shfl_xor_sync(0xffffffffu, gr, off);
+                    gi += __shfl_xor_sync(0xffffffffu, gi, off);
+                }
+            }
+            if (live) {
+                if (r == 0 && g == 0) {
+                    sig2[pid * w + p] = al;
+                    sig2[pid * w + q] = be;
+                }
+                Rot<T> R;
+                const int act = rot_params<T>(al, be, gr, gi, tol, R);
+                if (g == 0) {
+                    Prm<T> pm;
+                    pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
+                    prm[(r & 1) * w + k] = pm;
+                }
+                if (act < 0) {
+                    bad = true;
+                } else if (act > 0) {
+                    rot = true;
+#pragma unroll
+                    for (int i = 0; i < RPLX; ++i) rot_apply<T>(x[i], y[i], R);
+                    col_store<T, RPLX>(x, smem_u32(panel) + p * colb + g * T2SZ, rstride);
+                    col_store<T, RPLX>(y, smem_u32(panel) + q * colb + g * T2SZ, rstride);
+                }
+            }
+        } else if (active && r >= 1) {  // V warps: round r-1
+            const Prm<T> pm = prm[((r - 1) & 1) * w + k];
+            if (pm.act > 0) {
+                int p, q;
+                pair_cols(kk, r - 1, w, p, q);
+                Rot<T> R;
+                R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                T2 xv[RPLV], yv[RPLV];
+                const uint32_t ap = smem_u32(panel) + p * colb + g * T2SZ + voff_b;
+                const uint32_t aq = smem_u32(panel) + q * colb + g * T2SZ + voff_b;
+                col_load<T, RPLV>(xv, ap, rstride);
+                col_load<T, RPLV>(yv, aq, rstride);
+#pragma unroll
+                for (int i = 0; i < RPLV; ++i) rot_apply<T>(xv[i], yv[i], R);
+                col_store<T, RPLV>(xv, ap, rstride);
+                col_store<T, RPLV>(yv, aq, rstride);
+            }
+        }
+        __syncthreads();
+    }
+    return (rot ? 1 : 0) | (bad ? 2 : 0);
+}
+
+template <typename T, int C, int RPLX, int RPLV>
+__device__ __noinline__ int panel_cross_split(const JacShape &s, unsigned char *smem, int rank,
+                                              cplx_t<T> *Abuf, cplx_t<T> *Bbuf0, T tol) {
+    using T2 = cplx_t<T>;
+    const int w = s.P, G = s.G, LD = s.ldx, VOFF = s.ldv;
+    const int tid = threadIdx.x;
+    const bool xrole = tid < w * G;
+    const int ltid = xrole ? tid : tid - w * G;
+    const int k = ltid / G, g = ltid % G;
+    const bool active = k < w;
+    constexpr uint32_t T2SZ = sizeof(T2);
+    const uint32_t rstride = (uint32_t)G * T2SZ;
+    const uint32_t voff_b = (uint32_t)VOFF * T2SZ;
+    const uint32_t colb = (uint32_t)LD * T2SZ;
+    const uint32_t roff = xrole ? 0u : voff_b;  // this role's rows inside a column
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
+    Prm<T> *prm = reinterpret_cast<Prm<T> *>(smem + s.off_recv);
+    bool rot = false, bad = false;
+    int *pos = flags + 4;
+    const size_t panel_elems = (size_t)w * LD;
+    int bcur = flags[2];
+    T2 *Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
+    constexpr int RMAX = RPLX > RPLV ? RPLX : RPLV;
+    // stationary a column rows of this role (X rows or V rows) in registers
+    T2 ra[RMAX];
+    if (active) {
+        if (xrole) col_load<T, RPLX>(*reinterpret_cast<T2 (*)[RPLX]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ, rstride);
+        else col_load<T, RPLV>(*reinterpret_cast<T2 (*)[RPLV]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ + voff_b, rstride);
+    }
+#pragma unroll 1
+    for (int t = 0; t < 2 * C - 1; ++t) {
+#pragma unroll 1
+        for (int sr = 0; sr <= w; ++sr) {  // w rounds + 1 drain
+            if (xrole) {
+                T al = 0, be = 0, gr = 0, gi = 0;
+                T2 y[RPLX];
+                int j = k + sr;
+                if (j >= w) j -= w;
+                const bool live = active && sr < w;
+                const uint32_t ab = smem_u32(Bbuf) + j * colb + g * T2SZ;
+                if (live) {
+                    col_load<T, RPLX>(y, ab, rstride);
+#pragma unroll
+                    for (int i = 0; i < RPLX; ++i) {
+                        al = fma(ra[i].y, ra[i].y, fma(ra[i].x, ra[i].x, al));
+                        be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                        gr = fma(ra[i].y, y[i].y, fma(ra[i].x, y[i].x, gr));
+                        gi = fma(-ra[i].y, y[i].x, fma(ra[i].x, y[i].y, gi));
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    if (off < G) {
+                        al += __shfl_xor_sync(0xffffffffu, al, off);
+                        be += __shfl_xor_sync(0xffffffffu, be, off);
+                        gr += __shfl_xor_sync(0xffffffffu, gr, off);
+                        gi += __shfl_xor_sync(0xffffffffu, gi, off);
+                    }
+                }
+                if (live) {
+                    Rot<T> R;
+                    const int act = rot_params<T>(al, be, gr, gi, tol, R);
+                    if (g == 0) {
+                        Prm<T> pm;
+                        pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
+                        prm[(sr & 1) * w + k] = pm;
+                    }
+                    if (act < 0) {
+                        bad = true;
+                    } else if (act > 0) {
+                        rot = true;
+#pragma unroll
+                        for (int i = 0; i < RPLX; ++i) rot_apply<T>(ra[i], y[i], R);
+                        col_store<T, RPLX>(y, ab, rstride);
+                    }
+                }
+            } else if (active && sr >= 1) {  // V warps: round sr-1
+                const Prm<T> pm = prm[((sr - 1) & 1) * w + k];
+                if (pm.act > 0) {
+                    int j = k + sr - 1;
+                    if (j >= w) j -= w;
+                    Rot<T> R;
+                    R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                    T2 yv[RPLV];
+                    const uint32_t ab = smem_u32(Bbuf) + j * colb + g * T2SZ + voff_b;
+                    col_load<T, RPLV>(yv, ab, rstride);
+#pragma unroll
+                    for (int i = 0; i < RPLV; ++i) rot_apply<T>(ra[i], yv[i], R);
+                    col_store<T, RPLV>(yv, ab, rstride);
+                }
+            }
+            __syncthreads();
+        }
+        if constexpr (C > 1) {
+            if (t == 2 * C - 2) break;
+            // ---- panel rotation across the cluster (see panel_cross) ----------
+            if (active) {
+                if (xrole) col_store<T, RPLX>(*reinterpret_cast<T2 (*)[RPLX]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ, rstride);
+                else col_store<T, RPLV>(*reinterpret_cast<T2 (*)[RPLV]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ + voff_b, rstride);
+            }
+            cluster_sync_all();
+            cg::cluster_group cl = cg::this_cluster();
+            T2 *Bnext = Bbuf0 + (size_t)(bcur ^ 1) * panel_elems;
+            if (rank != 0 && active) {
+                const uint32_t src = (rank == C - 1) ? map_rank(smem_u32(Bbuf), rank)
+                                                     : map_rank(smem_u32(Abuf), rank + 1);
+                const uint32_t aa = src + k * colb + g * T2SZ + roff;
+                if (xrole) col_load_cluster<T, RPLX>(*reinterpret_cast<T2 (*)[RPLX]>(ra), aa, rstride);
+                else col_load_cluster<T, RPLV>(*reinterpret_cast<T2 (*)[RPLV]>(ra), aa, rstride);
+            }
+            {
+                const T2 *src;
+                if (rank == 0) src = cl.map_shared_rank(Abuf, 1);
+                else src = cl.map_shared_rank(Bbuf0 + (size_t)bcur * panel_elems, rank - 1);
+                const float4 *s4 = reinterpret_cast<const float4 *>(src);
+                float4 *d4 = reinterpret_cast<float4 *>(Bnext);
+                const size_t n4 = panel_elems * sizeof(T2) / sizeof(float4);
+                for (size_t x = tid; x < n4; x += blockDim.x) d4[x] = s4[x];
+            }
+            int np = 0;
+            if (tid < 2 * C) np = (tid == 0) ? pos[0] : (tid == 2 * C - 1 ? pos[1] : pos[tid + 1]);
+            cluster_sync_all();
+            if (tid < 2 * C) pos[tid] = np;
+            bcur ^= 1;
+            Bbuf = Bnext;
+            if (tid == 0) flags[2] = bcur;
+            __syncthreads();
+        }
+    }
+    if (active) {  // a rows back to shared memory
+        if (xrole) col_store<T, RPLX>(*reinterpret_cast<T2 (*)[RPLX]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ, rstride);
+        else col_store<T, RPLV>(*reinterpret_cast<T2 (*)[RPLV]>(ra), smem_u32(Abuf) + k * colb + g * T2SZ + voff_b, rstride);
+    }
+    return (rot ? 1 : 0) | (bad ? 2 : 0);
+}
+
+template <typename T, int C, int RPLX, int RPLV, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 1024 : JAC_MAX_THREADS)
 jacobi_panel_kernel(const JacArgs<T> a) {
     using T2 = cplx_t<T>;
     constexpr bool WANTV = RPLV > 0;
@@ -406,8 +648,14 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             __syncthreads();
             if (tid < 32) start_pos[tid] = pos[tid];
 
-            int fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
-            fl |= panel_cross<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+            int fl;
+            if constexpr (SPLIT) {
+                fl = panel_within_split<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
+                fl |= panel_cross_split<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+            } else {
+                fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
+                fl |= panel_cross<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+            }
             bcur = flags[2];
             Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
             const bool rot = fl & 1, bad = fl & 2;

@@ -77,6 +77,65 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
     return DeviceSpectrum(values, out.sigma, out.U, out.V, out.info, u0, count, dtype)
 
 
+def lfa_device_multi(layers, dtype: str, want_vectors: bool = False,
+                     tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
+                     timer: engine.Timer | None = None):
+    """Several layers in ONE batched SVD call (cfg4: 16 ResNet-18 layers).
+
+    ``layers`` = [(w_dev, n, m), ...].  K1 runs per layer, then a single
+    cs_batched_svd_grouped call solves every layer's representatives with
+    its own kernel configuration, the groups running concurrently on forked
+    streams so small and large shapes share the SMs."""
+    if timer:
+        timer.mark("t0")
+    fields = [engine.symbol_field(w, n, m, dtype, half=True) for w, n, m in layers]
+    if timer:
+        timer.mark("t1")
+    outs = engine.batched_svd_grouped(fields, dtype, want_vectors, tol, max_sweeps)
+    if timer:
+        timer.mark("t2")
+    res = []
+    for (w, n, m), o in zip(layers, outs):
+        vals = engine.spectrum_values(o.sigma, dtype, n, m, True)
+        res.append(DeviceSpectrum(vals, o.sigma, o.U, o.V, o.info, 0, o.sigma.shape[0], dtype))
+    if timer:
+        timer.mark("t3")
+    return res
+
+
+def compute_spectra(kernels, dims, values_only: bool = True, tol: float = DEFAULT_SVD_TOL,
+                    max_sweeps: int = DEFAULT_MAX_SWEEPS, *, device=None, dtype=None):
+    """``compute_spectrum`` for a list of layers in one batched device call
+    (extension: the reference solves one kernel per call).  ``dims`` is one
+    SpatialDims or one per kernel.  Returns a list of SpectrumResult."""
+    from .kernels import FrequencyGrid
+
+    kernels = list(kernels)
+    dims_l = list(dims) if isinstance(dims, (list, tuple)) else [dims] * len(kernels)
+    dev = engine.require_cuda(device)
+    dts = {_resolve_dtype(k, dtype) for k in kernels}
+    if len(dts) != 1:
+        raise ValueError("compute_spectra: all kernels must share one precision (pass dtype=)")
+    dt = dts.pop()
+    for k in kernels:
+        validate_kernel(k)
+    layers = [(engine.weights_to_device(k, dt, dev), d.n, d.m) for k, d in zip(kernels, dims_l)]
+    tm = engine.Timer(dev)
+    outs = lfa_device_multi(layers, dt, not values_only, tol, max_sweeps, timer=tm)
+    results = []
+    for k, d, o in zip(kernels, dims_l, outs):
+        f = engine.first_failure(o.info)
+        if f >= 0:
+            reps = engine.half_grid_indices(d.n, d.m)
+            engine.raise_convergence(int(reps[f]), FrequencyGrid(d).frequencies, max_sweeps)
+    timings = PhaseTimings.build(tm.seconds("t0", "t1"), tm.seconds("t1", "t3"), 0.0)
+    for k, d, o in zip(kernels, dims_l, outs):
+        results.append(SpectrumResult(values=o.values.cpu().numpy(), method="lfa",
+                                      boundary=PERIODIC, dims=d, channels=(k.c_in, k.c_out),
+                                      timings=timings))
+    return results
+
+
 def field_bytes(kernel_or_shape, n: int, m: int, dtype: str, want_vectors: bool) -> int:
     co, ci = kernel_or_shape
     esz = 8 if dtype == "f32" else 16
