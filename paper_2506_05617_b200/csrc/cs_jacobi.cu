@@ -123,7 +123,7 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     // with vectors, X and V rows go to separate warps when 2x the threads fit
     // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
     s.split = (wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&
-               rplx <= budget / 2 && std::getenv("CS_NO_SPLIT") == nullptr) ? 1 : 0;
+               rplx <= budget / 2 && std::getenv("CS_SPLIT") != nullptr) ? 1 : 0;  // opt-in: spills at 64 regs
     if (!s.split && rplx + rplv > budget) return false;
     s.G = G;
     s.RPL = rplx;
