@@ -161,6 +161,20 @@ int cs_spectrum_values(const void *sigma, int dtype, long long count, int r, int
                        int half_grid, double *values, void *workspace,
                        size_t workspace_bytes, void *stream);
 
+/* Global singular vector of the unrolled periodic operator for one frequency
+ * (grid indices fi, fj: k = (fi/n, fj/m)) and factor column `col` of `factor`
+ * ((rows, r) row-major, the frequency's U or V): out[(x1*n + x2)*rows + ch] =
+ * exp(2 pi i (k1 x2 + k2 x1))/sqrt(nm) factor[ch, col].  Replaces
+ * blocksvd.py:292-311 (materialize_singular_vector). */
+int cs_materialize_vector(const void *factor, int dtype, int rows, int r, int col, int fi,
+                          int fj, int n, int m, void *out, void *stream);
+
+/* Matrix-free periodic convolution y = A x on an n x m torus: x (m, n, c_in),
+ * y (m, n, c_out) complex, W (c_out, c_in, k_h, k_w) real; fp64 accumulation.
+ * Replaces explicit.py:149-178 (apply_conv_reference, periodic boundary). */
+int cs_apply_conv(const void *W, int dtype, int c_out, int c_in, int k_h, int k_w, int n, int m,
+                  const void *x, void *y, void *stream);
+
 /* Device microbenchmarks for the roofline denominators: achieved FP32 / FP64
  * FMA rate in flop/s over `ms` milliseconds of a dependent-FMA kernel. */
 double cs_measure_fma_peak(int dtype, int device);

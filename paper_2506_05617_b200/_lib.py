@@ -58,6 +58,8 @@ _SIGNATURES = {
     "cs_first_failure": (_i, [_vp, _ll, _vp, _vp]),
     "cs_spectrum_values_workspace": (_sz, [_ll, _i]),
     "cs_spectrum_values": (_i, [_vp, _i, _ll, _i, _i, _i, _i, _vp, _vp, _sz, _vp]),
+    "cs_materialize_vector": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "cs_apply_conv": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
     "cs_measure_fma_peak": (_d, [_i, _i]),
 }
 

@@ -192,10 +192,15 @@ def materialize_singular_vector(triplet: SvdTriplet, column: int, side: str,
     W = triplet.U if side == "left" else triplet.V
     if not 0 <= column < W.shape[1]:
         raise IndexOutOfRange(f"column {column} out of range for rank {W.shape[1]}")
-    if not isinstance(W, np.ndarray):
-        W = W.cpu().numpy()
     n, m = dims.n, dims.m
     k1, k2 = triplet.k
+    if not isinstance(W, np.ndarray):
+        # device factors: the vector is formed on the device (cs_materialize_vector)
+        fi, fj = int(round(float(k1) * n)) % n, int(round(float(k2) * m)) % m
+        if abs(fi - float(k1) * n) > 1e-9 * n or abs(fj - float(k2) * m) > 1e-9 * m:
+            raise ValueError("device materialisation needs a grid frequency")
+        dt = "f32" if W.dtype == engine.torch.complex64 else "f64"
+        return engine.materialize_vector(W, column, fi, fj, n, m, dt)
     x1, x2 = np.divmod(np.arange(n * m), n)
     wave = np.exp(2j * np.pi * (k1 * x2 + k2 * x1)) / np.sqrt(n * m)
     return (wave[:, None] * np.asarray(W)[None, :, column]).ravel()

@@ -484,6 +484,25 @@ class Timer:
         return self.events[a].elapsed_time(self.events[b]) / 1e3
 
 
+def materialize_vector(factor, col: int, fi: int, fj: int, n: int, m: int, dtype: str):
+    rows, r = factor.shape
+    out = torch.empty((n * m * rows,), dtype=complex_dtype(dtype), device=factor.device)
+    st = _lib.load().cs_materialize_vector(ptr(factor.contiguous()), dtype_code(dtype), rows, r,
+                                           col, fi, fj, n, m, ptr(out),
+                                           stream_ptr(factor.device))
+    _lib.check(st, "cs_materialize_vector")
+    return out
+
+
+def apply_conv(w_dev, x, n: int, m: int, dtype: str):
+    co, ci, kh, kw = w_dev.shape
+    y = torch.empty((m, n, co), dtype=complex_dtype(dtype), device=w_dev.device)
+    st = _lib.load().cs_apply_conv(ptr(w_dev), dtype_code(dtype), co, ci, kh, kw, n, m,
+                                   ptr(x.contiguous()), ptr(y), stream_ptr(w_dev.device))
+    _lib.check(st, "cs_apply_conv")
+    return y
+
+
 def fma_peak_flops(dtype: str = "f32", device_index: int = 0) -> float:
     """Measured FFMA/DFMA throughput (flop/s) for the roofline denominator."""
     return float(_lib.load().cs_measure_fma_peak(dtype_code(dtype), device_index))

@@ -139,3 +139,60 @@ def test_global_singular_vector_residual_cfg2(cuda):
             u = cs.materialize_singular_vector(t, col, "left", dims)
             Av = _apply_periodic_conv(w32.astype(np.float64), v).ravel()
             assert np.linalg.norm(Av - t.sigma[col] * u) <= 1e-5 * smax
+
+
+def test_device_materialize_matches_host(cuda):
+    kernel = cs.random_kernel(3, 2, 3, 3, seed=18)
+    dims = cs.SpatialDims(5, 4)
+    fld = cs.build_symbol_field(kernel, dims, return_device_tensors=True)
+    _, trip_dev = cs.spectrum_from_field(fld, values_only=False, return_device_tensors=True)
+    _, trip_host = cs.spectrum_from_field(fld, values_only=False)
+    for f in (0, 3, 7, 19):
+        for side in ("left", "right"):
+            d = cs.materialize_singular_vector(trip_dev[f], 1, side, dims).cpu().numpy()
+            h = cs.materialize_singular_vector(trip_host[f], 1, side, dims)
+            assert np.abs(d - h).max() <= 1e-14
+    # matrix-free operator vs the dense periodic matrix at a small size
+    from test_gpu_parity import _periodic_matrix
+
+    x = (np.random.default_rng(4).standard_normal((dims.m, dims.n, 2))
+         + 1j * np.random.default_rng(5).standard_normal((dims.m, dims.n, 2)))
+    y = cs.apply_conv(kernel, x, dims)
+    A = _periodic_matrix(kernel.weights, dims.n, dims.m)
+    assert np.abs(y.ravel() - A @ x.ravel()).max() <= 1e-12
+
+
+def test_global_singular_vector_residual_cfg5(cuda):
+    """||A v - sigma u|| on the 16.7M x 16.7M cfg5 operator, entirely on the device."""
+    layer = configs.WORKLOADS[5].layers[0]
+    w, res = _run(layer, True, cuda)
+    reps = engine.half_grid_indices(layer.n, layer.m)
+    smax = float(res.values[0])
+    for u in (0, 1, 128, 4000, 32769):
+        fi, fj = divmod(int(reps[u]), layer.m)
+        for col in (0, 100, 255):
+            s = float(res.sigma[u, col])
+            v = engine.materialize_vector(res.V[u], col, fi, fj, layer.n, layer.m, "f32")
+            uu = engine.materialize_vector(res.U[u], col, fi, fj, layer.n, layer.m, "f32")
+            Av = engine.apply_conv(w, v.reshape(layer.m, layer.n, -1), layer.n, layer.m, "f32")
+            r = torch.linalg.vector_norm(Av.reshape(-1) - s * uu).item()
+            assert r <= 1e-5 * smax, (u, col, r)
+
+
+@pytest.mark.parametrize("key", ["cfg2_l0", "cfg3_l0", "cfg4_l0", "cfg4_l4", "cfg4_l8",
+                                 "cfg4_l12", "cfg5_l0"])
+def test_fp64_sampled_frequencies(cuda, golden, key):
+    """fp64 parity mode (1e-10 per frequency) on every config's sampled
+    frequencies: explicit-frequency K1 (cs_symbol_at) + fp64 Jacobi."""
+    c, li = int(key[3]), int(key.split("_l")[1])
+    layer = configs.WORKLOADS[c].layers[li]
+    fidx = golden[key + "_fidx"]
+    kernel = cs.ConvKernel.from_array(configs.layer_weights(layer).astype(np.float64))
+    w = engine.weights_to_device(kernel, "f64", cuda)
+    grid = cs.FrequencyGrid(cs.SpatialDims(layer.n, layer.m)).frequencies
+    blocks = engine.symbol_at_freqs(w, grid[fidx], "f64")
+    bn = torch.linalg.matrix_norm(blocks).cpu().numpy()
+    assert np.allclose(bn, golden[key + "_blocknorm"], rtol=1e-13, atol=0)
+    out = engine.batched_svd(blocks, "f64", False)
+    assert (out.info.cpu().numpy() > 0).all()
+    assert per_freq_rel_err(out.sigma.cpu().numpy(), golden[key + "_sigma"]).max() <= 1e-10
