@@ -214,7 +214,7 @@ def run_reference(args, wl, rank):
         "metric": "singular values/sec (full conv SVD, device-timed)", "value": value,
         "unit": "singular values/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Philox He-normal fp32 weights)", "impl": "reference",
         "config": workload_config(wl, args.gpus),
         "cpu_baseline": {"value": value, "unit": "singular values/s", "cores": threads,
@@ -270,7 +270,7 @@ def run_ours(args, wl, rank, world, local_rank):
         for i, (l, w) in enumerate(zip(layers, w_dev)):
             tm = timers[i] if timers else None
             if world > 1:
-                outs.append(lfa_sharded(w, l.n, l.m, dt, wl.vectors))
+                outs.append(lfa_sharded(w, l.n, l.m, dt, wl.vectors, timer=tm))
             else:
                 outs.append(cs.lfa_device(w, l.n, l.m, dt, wl.vectors, timer=tm))
         return outs
@@ -299,7 +299,7 @@ def run_ours(args, wl, rank, world, local_rank):
         timers = [[engine.Timer(dev)] for _ in range(args.steps)]
     ev[0].record(stream)
     for s in range(args.steps):
-        outs = step(timers[s] if world == 1 else None)
+        outs = step(timers[s])
         ev[s + 1].record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -315,8 +315,9 @@ def run_ours(args, wl, rank, world, local_rank):
 
     # per-phase / per-kernel device times (1 GPU: events inside the step)
     roofline = None
+    roofline_k1 = None
     phases = None
-    if world == 1:
+    if True:  # per-rank phases; at N > 1 the work below is this rank's share
         k1 = [tm.seconds("t0", "t1") for row in timers for tm in row if "t0" in tm.events]
         sv = [tm.seconds("t1", "t2") for row in timers for tm in row if "t0" in tm.events]
         asm = [tm.seconds("t2", "t3") for row in timers for tm in row if "t0" in tm.events]
@@ -324,7 +325,9 @@ def run_ours(args, wl, rank, world, local_rank):
         phases = {"assembly_K1_ms": 1e3 * sum(k1) / args.steps,
                   "svd_ms": 1e3 * sum(sv) / args.steps,
                   "spectrum_sort_ms": 1e3 * sum(asm) / args.steps}
-        svd_flops_step = sum(svd_flops(l, wl.vectors) for l in layers)
+        shares = [(shard_range(half_count(l.n, l.m), rank, world)[1] if world > 1 else None)
+                  for l in layers]
+        svd_flops_step = sum(svd_flops(l, wl.vectors, c) for l, c in zip(layers, shares))
         svd_s = sum(sv) / args.steps
         achieved = svd_flops_step / svd_s / 1e12
         roofline = {"kernel": "jacobi_panel_kernel (K2/K3 batched one-sided Jacobi; SVD phase "
@@ -336,7 +339,7 @@ def run_ours(args, wl, rank, world, local_rank):
                                    "dependent-FFMA probe); MEASURED_PEAKS.json holds no FP32 peak",
                     "algorithmic": "Golub-Reinsch sigma+U+V count x4 complex per unique block "
                                    "(SURVEY 8(d)); Jacobi executes ~3.5x more"}
-        asm_b = sum(asm_bytes(l) for l in layers)
+        asm_b = sum(asm_bytes(l, c) for l, c in zip(layers, shares))
         hbm = peaks.get("hbm_gbs", 6650.0)
         k1_s = sum(k1) / args.steps
         roofline_k1 = {"kernel": "symbol_rows_kernel (K1 half-grid assembly)", "bound": "hbm",
@@ -411,11 +414,11 @@ def run_ours(args, wl, rank, world, local_rank):
             "metric": "singular values/sec (full conv SVD, device-timed)",
             "value": value, "unit": "singular values/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox He-normal fp32 weights, BASELINE.json configs)",
             "config": workload_config(wl, world),
-            "roofline": roofline, "roofline_assembly": roofline_k1 if world == 1 else None,
+            "roofline": roofline, "roofline_assembly": roofline_k1,
             "phases": phases, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "sweeps_mean": sweeps_mean, "converged": ok,
             "step_ms": step_ms,

@@ -197,6 +197,9 @@ static bool plan_generic(int co, int ci, bool wantv, int C, bool smem_resident, 
 template <typename T>
 static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     const int Cs[5] = {1, 2, 4, 8, 16};
+    if (const char *fc = std::getenv("CS_PANEL_C")) {  // experiment hook: force the cluster size
+        if (plan_panel<T>(co, ci, wantv, std::atoi(fc), s)) return true;
+    }
     for (int i = 0; i < 5; ++i) {
         if (!plan_panel<T>(co, ci, wantv, Cs[i], s)) continue;
         int j = i;

@@ -46,7 +46,7 @@ def gather_sigma(sigma, total: int, group=None):
 
 def lfa_sharded(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
                 tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
-                group=None, assemble: bool = True) -> DeviceSpectrum:
+                group=None, assemble: bool = True, timer=None) -> DeviceSpectrum:
     """This rank's share of the LFA solve plus (optionally) the full spectrum.
 
     Returns the local DeviceSpectrum (sigma/U/V/info of its representatives)
@@ -58,8 +58,10 @@ def lfa_sharded(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
     total = engine.half_grid_count(n, m)
     u0, cnt = shard_range(total, rank, world)
     res = lfa_device(w_dev, n, m, dtype, want_vectors, tol, max_sweeps, u0=u0, count=cnt,
-                     assemble=(world == 1 and assemble))
+                     assemble=(world == 1 and assemble), timer=timer)
     if world > 1 and assemble:
         full = gather_sigma(res.sigma, total, group)
         res.values = engine.spectrum_values(full, dtype, n, m, True)
+        if timer:
+            timer.mark("t3")  # assembly now includes the all-gather
     return res

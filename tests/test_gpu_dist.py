@@ -1,0 +1,75 @@
+"""Frequency-sharded solve (distributed.lfa_sharded) with 2 ranks on one GPU.
+
+The only GPU available to this run is cuda:0, so both ranks use it and the
+sigma all-gather runs over gloo (host-mediated).  Nothing on the device waits
+for the other rank: each rank solves its own representative range, then the
+collective exchanges the sigma shards -- the same code path NCCL runs on a
+multi-GPU node.  The assembled spectrum must equal the single-rank one.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cfg, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2506_05617_b200 import configs
+    from paper_2506_05617_b200.distributed import lfa_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    layer = configs.WORKLOADS[cfg].layers[0]
+    w = torch.from_numpy(configs.layer_weights(layer)).cuda()
+    res = lfa_sharded(w, layer.n, layer.m, "f32", configs.WORKLOADS[cfg].vectors)
+    q.put((rank, res.u0, res.count, res.values.cpu().numpy(), res.sigma.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_two_ranks_match_single(cuda, cfg):
+    from paper_2506_05617_b200 import configs
+    from paper_2506_05617_b200.pipeline import lfa_device
+
+    layer = configs.WORKLOADS[cfg].layers[0]
+    w = torch.from_numpy(configs.layer_weights(layer)).to(cuda)
+    single = lfa_device(w, layer.n, layer.m, "f32", configs.WORKLOADS[cfg].vectors)
+    ref_vals = single.values.cpu().numpy()
+    ref_sig = single.sigma.cpu().numpy()
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(g, 2, port, cfg, q)) for g in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    outs.sort(key=lambda o: o[0])
+    assert outs[0][1] == 0 and outs[0][1] + outs[0][2] == outs[1][1]
+    for _, u0, cnt, vals, sig in outs:
+        assert np.abs(vals - ref_vals).max() <= 2e-6 * ref_vals[0]
+        assert np.abs(sig - ref_sig[u0:u0 + cnt]).max() <= 2e-6 * ref_vals[0]
