@@ -136,8 +136,14 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     off = align16(off + s.ncp * sizeof(T));
     s.off_perm = off;
     off = align16(off + 2 * s.ncp * sizeof(int));
-    s.off_send = off;  // staging for the cluster norm gather
-    off = align16(off + s.ncp * sizeof(T));
+    s.off_send = off;  // staging for the cluster norm gather; Gram mode: G and D
+    // Gram-blocked cross phase (opt-in CS_GRAM=1: correct, but 2.8x slower than the
+    // scalar cross rounds on cfg5 in SIMT; kept as the skeleton for a tensor-core version)
+    const char *genv = std::getenv("CS_GRAM");
+    s.gram = (sizeof(T) == 4 && w == 16 && !s.split && genv != nullptr && genv[0] == '1' &&
+              w * (s.mr + s.Rv) <= 16 * s.threads) ? 1 : 0;  // a-panel staging: 16 per thread
+    const size_t gbytes = s.gram ? 2 * (size_t)(2 * w) * (2 * w + 1) * 2 * sizeof(T) : 0;
+    off = align16(off + std::max(s.ncp * sizeof(T), gbytes));
     s.off_recv = off;  // split mode: rotation parameters [2][w]
     off = align16(off + 2 * (size_t)w * 4 * sizeof(T) + 64);
     s.off_mbar = off;  // sweep flags + panel position tables

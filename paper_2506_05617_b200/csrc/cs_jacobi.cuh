@@ -44,6 +44,7 @@ struct JacShape {
     size_t off_sig, off_perm, off_send, off_recv, off_mbar, off_x, off_v, smem;
     int smem_resident;
     int split;  // panel kernel: separate X and V warps (2x threads)
+    int gram;   // panel kernel: Gram-blocked cross phase
     long long num_clusters;
     size_t scratch_per_cta;  // complex elements, generic global-memory mode
 };

@@ -558,6 +558,280 @@ __device__ __noinline__ int panel_cross_split(const JacShape &s, unsigned char *
     return (rot ? 1 : 0) | (bad ? 2 : 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// Gram-blocked cross phase ("blocked variant": the O(rows) work of a whole
+// super-round becomes two GEMM-shaped passes).  Per super-round:
+//   1. G = P^H P over the X rows of the CTA's two panels P = [a b] (2w x 2w,
+//      Hermitian, 4x4 register tiles, row chunks reduced by warp shuffles);
+//   2. the same w cross rounds of rotations run on G (two-sided: columns,
+//      then rows) while D = Q - I accumulates the product Q of the rotations
+//      (D <- D J + (J - I));
+//   3. P <- P + P D for all X and V rows (register-streamed, in place).
+// In exact arithmetic the rotations are those of the one-sided sweep; a
+// rotation-free sweep makes no update, so convergence is still certified on
+// freshly formed dot products.  The (Q - I) form keeps the rounding of the
+// update relative to the (small) correction, as rot_apply does per rotation.
+// Used when the 2w x 2w G and D fit next to the panels (w <= 16).
+// ---------------------------------------------------------------------------
+// phase 1: G = P^H P over the X rows (upper 4x4 tiles, 8 row chunks per tile
+// reduced with warp shuffles); also clears D
+template <typename T>
+__device__ __noinline__ void gram_phase(unsigned char *smem, uint32_t abase, uint32_t bbase,
+                                        int w, int LD, int mr, cplx_t<T> *Gm, cplx_t<T> *Dm) {
+    using T2 = cplx_t<T>;
+    const int n2 = 2 * w, ldg = n2 + 1, tid = threadIdx.x;
+    const int ntile = n2 / 4, nup = ntile * (ntile + 1) / 2;
+    const int chunk = tid & 7, tslot = tid >> 3;
+    int ti = 0, tj = 0;
+    const bool tact = tslot < nup;
+    if (tact) {
+        int rem = tslot;
+        while (rem >= ntile - ti) { rem -= ntile - ti; ++ti; }
+        tj = ti + rem;
+    }
+    T gr[4][4], gi[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) gr[a][b] = gi[a][b] = (T)0;
+    if (tact) {
+        const int rows_per = (mr + 7) / 8;
+        const int r0 = chunk * rows_per, r1 = min(mr, r0 + rows_per);
+        const uint32_t colb = (uint32_t)LD * sizeof(T2);
+        auto cbase = [&](int c) -> uint32_t { return c < w ? abase + c * colb : bbase + (c - w) * colb; };
+        const uint32_t i0 = cbase(ti * 4), j0 = cbase(tj * 4);
+        const bool icont = (ti * 4 + 3 < w) || (ti * 4 >= w);  // 4 columns in one panel
+        const bool jcont = (tj * 4 + 3 < w) || (tj * 4 >= w);
+        for (int r = r0; r < r1; ++r) {
+            T2 xi[4], xj[4];
+            const uint32_t ro = (uint32_t)r * sizeof(T2);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                xi[a] = SmemIO<T>::ld((icont ? i0 + a * colb : cbase(ti * 4 + a)) + ro);
+                xj[a] = SmemIO<T>::ld((jcont ? j0 + a * colb : cbase(tj * 4 + a)) + ro);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {  // conj(xi) * xj
+                    gr[a][b] = fma(xi[a].y, xj[b].y, fma(xi[a].x, xj[b].x, gr[a][b]));
+                    gi[a][b] = fma(-xi[a].y, xj[b].x, fma(xi[a].x, xj[b].y, gi[a][b]));
+                }
+        }
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                gr[a][b] += __shfl_xor_sync(0xffffffffu, gr[a][b], off);
+                gi[a][b] += __shfl_xor_sync(0xffffffffu, gi[a][b], off);
+            }
+    if (tact && chunk == 0) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int i = ti * 4 + a, j = tj * 4 + b;
+                Gm[(size_t)i * ldg + j] = mk<T>(gr[a][b], gi[a][b]);
+                Gm[(size_t)j * ldg + i] = mk<T>(gr[a][b], -gi[a][b]);
+            }
+    }
+    for (int x = tid; x < n2 * n2; x += blockDim.x) Dm[(size_t)(x / n2) * ldg + (x % n2)] = mk<T>(0, 0);
+}
+
+// phase 2: the w cross rounds of rotations on G (two-sided), D <- D J + (J - I)
+template <typename T>
+__device__ __noinline__ int inner_phase(int w, cplx_t<T> *Gm, cplx_t<T> *Dm, Prm<T> *prm, T tol) {
+    using T2 = cplx_t<T>;
+    const int n2 = 2 * w, ldg = n2 + 1, tid = threadIdx.x, NT = blockDim.x;
+    bool rot = false, bad = false;
+#pragma unroll 1
+    for (int sr = 0; sr < w; ++sr) {
+        if (tid < w) {
+            const int p = tid, q = w + ((tid + sr) % w);
+            const T2 gpq = Gm[(size_t)p * ldg + q];
+            Rot<T> R;
+            const int act = rot_params<T>(Gm[(size_t)p * ldg + p].x, Gm[(size_t)q * ldg + q].x,
+                                          gpq.x, gpq.y, tol, R);
+            Prm<T> pm;
+            pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
+            prm[tid] = pm;
+            if (act < 0) bad = true;
+            if (act > 0) rot = true;
+        }
+        __syncthreads();
+        for (int x = tid; x < w * n2; x += NT) {  // columns p,q of G and D
+            const int k = x / n2, i = x % n2;
+            const Prm<T> pm = prm[k];
+            if (pm.act <= 0) continue;
+            const int p = k, q = w + ((k + sr) % w);
+            Rot<T> R;
+            R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+            T2 *gp = Gm + (size_t)i * ldg + p, *gq = Gm + (size_t)i * ldg + q;
+            T2 u = *gp, v = *gq;
+            rot_apply<T>(u, v, R);
+            *gp = u; *gq = v;
+            T2 *dp = Dm + (size_t)i * ldg + p, *dq = Dm + (size_t)i * ldg + q;
+            u = *dp; v = *dq;
+            rot_apply<T>(u, v, R);
+            // + (J - I): J_pp = J_qq = 1 + cm1, J_qp = -conj(s ph), J_pq = s ph
+            if (i == p) { u.x += R.cm1; v.x += R.wr; v.y += R.wi; }
+            if (i == q) { u.x -= R.wr; u.y += R.wi; v.x += R.cm1; }
+            *dp = u; *dq = v;
+        }
+        __syncthreads();
+        for (int x = tid; x < w * n2; x += NT) {  // rows p,q of G: J^H G
+            const int k = x / n2, j = x % n2;
+            const Prm<T> pm = prm[k];
+            if (pm.act <= 0) continue;
+            const int p = k, q = w + ((k + sr) % w);
+            Rot<T> R;
+            R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+            T2 *gp = Gm + (size_t)p * ldg + j, *gq = Gm + (size_t)q * ldg + j;
+            T2 u = *gp, v = *gq;
+            u.y = -u.y; v.y = -v.y;
+            rot_apply<T>(u, v, R);
+            u.y = -u.y; v.y = -v.y;
+            *gp = u; *gq = v;
+        }
+        __syncthreads();
+    }
+    return (rot ? 1 : 0) | (bad ? 2 : 0);
+}
+
+// phase 3: P <- P + P D for X rows and V rows, in place.  Two lanes per row
+// (each producing half of the 2w outputs) read the whole row before writing.
+template <typename T, int W>
+__device__ __noinline__ void update_phase(uint32_t abase, uint32_t bbase, int LD, int mr,
+                                          int nvr, int VOFF, const cplx_t<T> *Dm) {
+    using T2 = cplx_t<T>;
+    constexpr int w = W, n2 = 2 * W, ldg = n2 + 1;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const uint32_t colb = (uint32_t)LD * sizeof(T2);
+    const int nrows = mr + nvr;
+    for (int item = tid; item < 2 * ((nrows + 15) & ~15); item += NT) {
+        const int rr = item >> 1, h = item & 1;
+        const bool live = rr < nrows;
+        const int row = rr < mr ? rr : VOFF + (rr - mr);
+        const uint32_t ro = (uint32_t)row * sizeof(T2);
+        T2 acc[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) acc[c] = mk<T>(0, 0);
+        if (live) {
+#pragma unroll 2
+            for (int kk = 0; kk < n2; ++kk) {
+                const uint32_t ca = kk < w ? abase + kk * colb : bbase + (kk - w) * colb;
+                const T2 xv = SmemIO<T>::ld(ca + ro);
+                const T2 *dk = Dm + (size_t)kk * ldg + h * w;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const T2 d = dk[c];
+                    acc[c].x = fma(xv.x, d.x, fma(-xv.y, d.y, acc[c].x));
+                    acc[c].y = fma(xv.x, d.y, fma(xv.y, d.x, acc[c].y));
+                }
+            }
+        }
+        __syncwarp();  // the partner lane (other half of this row) has read the row
+        if (live) {
+            const uint32_t cb = h == 0 ? abase : bbase;
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                const uint32_t a = cb + c * colb + ro;
+                T2 v = SmemIO<T>::ld(a);
+                v.x += acc[c].x;
+                v.y += acc[c].y;
+                SmemIO<T>::st(a, v);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// the Gram-blocked cross phase (see the comment block above)
+template <typename T, int C, int RPLX, int RPLV>
+__device__ __noinline__ int panel_cross_gram(const JacShape &s, unsigned char *smem, int rank,
+                                             cplx_t<T> *Abuf, cplx_t<T> *Bbuf0, T tol) {
+    using T2 = cplx_t<T>;
+    const int w = s.P, LD = s.ldx, VOFF = s.ldv;
+    const int n2 = 2 * w, ldg = n2 + 1;
+    const int mr = s.mr, nvr = s.Rv;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
+    int *pos = flags + 4;
+    T2 *Gm = reinterpret_cast<T2 *>(smem + s.off_send);
+    T2 *Dm = Gm + (size_t)n2 * ldg;
+    Prm<T> *prm = reinterpret_cast<Prm<T> *>(smem + s.off_recv);
+    int fl = 0;
+    const size_t panel_elems = (size_t)w * LD;
+    int bcur = flags[2];
+    T2 *Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
+#pragma unroll 1
+    for (int t = 0; t < 2 * C - 1; ++t) {
+        gram_phase<T>(smem, smem_u32(Abuf), smem_u32(Bbuf), w, LD, mr, Gm, Dm);
+        __syncthreads();
+        const int f = inner_phase<T>(w, Gm, Dm, prm, tol);
+        fl |= f;
+        if (__syncthreads_or(f & 1)) {
+            update_phase<T, 16>(smem_u32(Abuf), smem_u32(Bbuf), LD, mr, nvr, VOFF, Dm);
+        }
+        __syncthreads();
+        if constexpr (C > 1) {
+            if (t == 2 * C - 2) break;
+            // panel rotation; the new a panel is staged through registers because
+            // peers read this CTA's Abuf until the second cluster sync
+            cluster_sync_all();
+            cg::cluster_group cl = cg::this_cluster();
+            T2 *Bnext = Bbuf0 + (size_t)(bcur ^ 1) * panel_elems;
+            constexpr int STAGE = 16;
+            T2 stage[STAGE];
+            const int rows_real = mr + nvr;  // real rows per column (X then V)
+            auto real_row = [&](int r) { return r < mr ? r : VOFF + (r - mr); };
+            if (rank != 0) {
+                const T2 *src = (rank == C - 1) ? Bbuf : cl.map_shared_rank(Abuf, rank + 1);
+#pragma unroll
+                for (int i = 0; i < STAGE; ++i) {
+                    const int x = tid + i * NT;
+                    if (x < w * rows_real) {
+                        const int c = x / rows_real, r = real_row(x % rows_real);
+                        stage[i] = src[(size_t)c * LD + r];
+                    }
+                }
+            }
+            {
+                const T2 *src;
+                if (rank == 0) src = cl.map_shared_rank(Abuf, 1);
+                else src = cl.map_shared_rank(Bbuf0 + (size_t)bcur * panel_elems, rank - 1);
+                const float4 *s4 = reinterpret_cast<const float4 *>(src);
+                float4 *d4 = reinterpret_cast<float4 *>(Bnext);
+                const size_t n4 = panel_elems * sizeof(T2) / sizeof(float4);
+                for (size_t x = tid; x < n4; x += NT) d4[x] = s4[x];
+            }
+            int np = 0;
+            if (tid < 2 * C) np = (tid == 0) ? pos[0] : (tid == 2 * C - 1 ? pos[1] : pos[tid + 1]);
+            cluster_sync_all();
+            if (rank != 0) {
+#pragma unroll
+                for (int i = 0; i < STAGE; ++i) {
+                    const int x = tid + i * NT;
+                    if (x < w * rows_real) {
+                        const int c = x / rows_real, r = real_row(x % rows_real);
+                        Abuf[(size_t)c * LD + r] = stage[i];
+                    }
+                }
+            }
+            if (tid < 2 * C) pos[tid] = np;
+            bcur ^= 1;
+            Bbuf = Bnext;
+            if (tid == 0) flags[2] = bcur;
+            __syncthreads();
+        }
+    }
+    return fl;
+}
+
 template <typename T, int C, int RPLX, int RPLV, bool SPLIT>
 __global__ void __launch_bounds__(SPLIT ? 1024 : JAC_MAX_THREADS)
 jacobi_panel_kernel(const JacArgs<T> a) {
@@ -652,6 +926,9 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             if constexpr (SPLIT) {
                 fl = panel_within_split<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
                 fl |= panel_cross_split<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+            } else if (s.gram) {
+                fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
+                fl |= panel_cross_gram<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
             } else {
                 fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
                 fl |= panel_cross<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
