@@ -582,7 +582,10 @@ __device__ __noinline__ void gram_phase(unsigned char *smem, uint32_t abase, uin
     using T2 = cplx_t<T>;
     const int n2 = 2 * w, ldg = n2 + 1, tid = threadIdx.x;
     const int ntile = n2 / 4, nup = ntile * (ntile + 1) / 2;
-    const int chunk = tid & 7, tslot = tid >> 3;
+    // warp-uniform trip count: every lane runs the same iterations (shuffles)
+    for (int base = 0; base < nup * 8; base += (int)blockDim.x) {
+    const int item = base + tid;
+    const int chunk = item & 7, tslot = item >> 3;
     int ti = 0, tj = 0;
     const bool tact = tslot < nup;
     if (tact) {
@@ -638,6 +641,7 @@ __device__ __noinline__ void gram_phase(unsigned char *smem, uint32_t abase, uin
                 Gm[(size_t)i * ldg + j] = mk<T>(gr[a][b], gi[a][b]);
                 Gm[(size_t)j * ldg + i] = mk<T>(gr[a][b], -gi[a][b]);
             }
+    }
     }
     for (int x = tid; x < n2 * n2; x += blockDim.x) Dm[(size_t)(x / n2) * ldg + (x % n2)] = mk<T>(0, 0);
 }

@@ -9,6 +9,7 @@ fp64; the reference's own unit-test tolerances where those are tighter
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2506_05617_b200 as cs
 from paper_2506_05617_b200 import configs, engine
@@ -344,3 +345,25 @@ def test_materialize_orthonormal_and_range(cuda):
             assert abs(np.vdot(vecs[a], vecs[b]) - (1.0 if a == b else 0.0)) < 1e-10
     with pytest.raises(cs.IndexOutOfRange):
         cs.materialize_singular_vector(trip[0], 3, "left", dims)
+
+
+@pytest.mark.parametrize("flag,shape,count", [("CS_GRAM", (32, 32), 320), ("CS_GRAM", (256, 256), 40),
+                                              ("CS_SPLIT", (64, 64), 320)])
+def test_opt_in_kernel_variants_match_oracle(cuda, orc, monkeypatch, flag, shape, count):
+    """The opt-in Gram-blocked and split-role panel variants (DESIGN.md 3);
+    batch sizes keep the planner on the panel widths those variants need."""
+    co, ci = shape
+    rng = np.random.default_rng(co + ci)
+    A = (rng.standard_normal((count, co, ci)) + 1j * rng.standard_normal((count, co, ci))) / np.sqrt(ci)
+    blocks = torch.from_numpy(A.astype(np.complex64)).to(cuda)
+    monkeypatch.setenv(flag, "1")
+    out = engine.batched_svd(blocks, "f32", True)
+    monkeypatch.delenv(flag)
+    ref, _ = orc.svd_values(A)
+    assert (out.info.cpu().numpy() > 0).all()
+    assert per_freq_rel_err(out.sigma.cpu().numpy(), ref).max() <= TOL32
+    U = out.U.cpu().numpy().astype(np.complex128)
+    V = out.V.cpu().numpy().astype(np.complex128)
+    s = out.sigma.cpu().numpy().astype(np.float64)
+    for f in range(0, count, max(1, count // 12)):
+        assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= 1e-5 * s[f][0]
