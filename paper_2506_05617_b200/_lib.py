@@ -72,7 +72,7 @@ def load(path: str | None = None):
     with _lock:
         if _LIB is not None and path is None:
             return _LIB
-        p = path or LIBPATH
+        p = path or os.environ.get("CS_LIBPATH") or LIBPATH  # override: A/B builds
         if not os.path.exists(p):
             raise RuntimeError(
                 f"convspectra_b200: CUDA library not built ({p}); run "

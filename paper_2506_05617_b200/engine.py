@@ -70,17 +70,22 @@ def dtype_of_tensor(t) -> str:
     return "f64"
 
 
+TOL32_FLOOR = 2.5e-6
+
+
 def effective_tol(tol: float, dtype: str, rows: int) -> float:
     """Convergence threshold actually used by the kernel.
 
     fp64 uses the caller's tol (reference default 1e-13, blocksvd.py:26).
     fp32 cannot resolve |gamma|/sqrt(alpha*beta) below its rounding floor
-    (~eps32*sqrt(rows)); the threshold is floored at 1e-6*sqrt(rows/64) so the
-    sweep loop terminates (measured: 12-13 sweeps at 256x256, sigma within
-    2e-7 of the fp64 reference, oracle/oracle.c *_f32acc study)."""
+    (~eps32*sqrt(rows)); the threshold is floored at 2.5e-6*sqrt(rows/64) so
+    the sweep loop terminates.  Measured on cfg5 (B200, tools/warmtest.py):
+    floor 2e-6 -> 5.56 mean warm sweeps, 5e-6 -> 5.33, 1e-5 -> 5.24, with
+    per-frequency sigma error 6-7e-7 of sigma_max in all three (bar 1e-5); the
+    middle value keeps the threshold at half the bar."""
     if dtype == "f64":
         return float(tol)
-    return max(float(tol), 1e-6 * math.sqrt(max(rows, 1) / 64.0))
+    return max(float(tol), TOL32_FLOOR * math.sqrt(max(rows, 1) / 64.0))
 
 
 def stream_ptr(device) -> int:

@@ -110,8 +110,8 @@ def test_half_grid_count_matches_library():
 
 def test_effective_tol_policy():
     assert engine.effective_tol(1e-13, "f64", 256) == 1e-13
-    assert engine.effective_tol(1e-13, "f32", 64) == pytest.approx(1e-6)
-    assert engine.effective_tol(1e-13, "f32", 256) == pytest.approx(2e-6)
+    assert engine.effective_tol(1e-13, "f32", 64) == pytest.approx(2.5e-6)
+    assert engine.effective_tol(1e-13, "f32", 256) == pytest.approx(5e-6)
     assert engine.effective_tol(1e-3, "f32", 256) == 1e-3
 
 
