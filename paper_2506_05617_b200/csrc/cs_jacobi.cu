@@ -16,6 +16,11 @@
 #include "cs_jacobi.cuh"
 #include "cs_panel.cuh"
 
+// debugging only: per-CTA progress codes written by the panel kernel into
+// mapped (pinned) host memory, readable while a kernel hangs
+static int *g_debug_progress = nullptr;
+extern "C" void cs_debug_progress(void *p) { g_debug_progress = (int *)p; }
+
 namespace cs {
 
 static int pow2ceil(int x) {
@@ -156,6 +161,9 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     s.smem = off;
     s.smem_resident = 1;
     s.nbuf = 1;
+    const char *gc = std::getenv("CS_GRAM_CHECK");  // default on; "0" = rotation-free sweep
+    // "2" (timing experiment): check after every rotating sweep, ignore the verdict
+    s.gcheck = (!s.split && !s.gram && !(gc && gc[0] == '0')) ? ((gc && gc[0] == '2') ? 2 : 1) : 0;
     return s.smem <= JAC_SMEM_LIMIT;
 }
 
@@ -278,6 +286,7 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
     a.ci = ci;
     a.tol = (T)tol;
     a.max_sweeps = max_sweeps;
+    a.dbg = g_debug_progress;
     a.sigma = (T *)sigma;
     a.info = info;
     a.zero_sigma = zero_sigma;

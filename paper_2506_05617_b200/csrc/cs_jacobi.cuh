@@ -45,6 +45,7 @@ struct JacShape {
     int smem_resident;
     int split;  // panel kernel: separate X and V warps (2x threads)
     int gram;   // panel kernel: Gram-blocked cross phase
+    int gcheck; // panel kernel: Gram convergence check instead of the rotation-free sweep
     long long num_clusters;
     size_t scratch_per_cta;  // complex elements, generic global-memory mode
 };
@@ -68,6 +69,7 @@ template <typename T> struct JacArgs {
     const cplx_t<T> *initX;
     const cplx_t<T> *initV;
     const long long *initV_index;
+    int *dbg;  // debugging only: per-CTA progress codes in mapped host memory (null = off)
 };
 
 // ---------------------------------------------------------------------------
@@ -113,6 +115,9 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// .aligned barriers need the whole warp converged at the instruction; inline
+// asm is opaque to the compiler's reconvergence, so converge explicitly
+// (without it the Gram check's <C=4, RPLX=8> instantiation hung).
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -143,6 +148,13 @@ template <typename T> struct Rot { T cm1, wr, wi; };
 // 0: skip, 1: rotate (params in R), -1: non-finite input.
 // The skip test compares squares (|gamma|^2 <= tol^2 alpha beta), so most
 // late-sweep pairs cost no sqrt at all.
+// Rotation parameters of the pair (alpha, beta, gamma = gr + i gi).  Returns
+// -1 non-finite, 0 below the threshold (no rotation), 1 rotate, 2 rotate with
+// |gamma|/sqrt(alpha beta) > GCHECK_TAU: the panel kernel runs its Gram
+// convergence check only after sweeps without such a pair (quadratic
+// convergence makes the next sweep likely rotation-free, tools/stopstudy.py).
+constexpr double GCHECK_TAU2 = 0.05 * 0.05;
+
 template <typename T>
 __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> &R) {
     if (!(dfinite(al) && dfinite(be) && dfinite(gr) && dfinite(gi))) return -1;
@@ -158,7 +170,7 @@ __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> 
     const T s = t / r;
     R.wr = s * (gr / ag);
     R.wi = s * (gi / ag);
-    return 1;
+    return q > (T)GCHECK_TAU2 * (al * be) ? 2 : 1;
 }
 
 // fp32: MUFU rsqrt + one Newton step and __fdividef -- no IEEE div/sqrt
@@ -191,7 +203,7 @@ __device__ __forceinline__ int rot_params<float>(float al, float be, float gr, f
     const float s = t * ir;
     R.wr = s * gr * inv_ag;
     R.wi = s * gi * inv_ag;
-    return 1;
+    return q > (float)GCHECK_TAU2 * (al * be) ? 2 : 1;
 }
 
 // x <- x + ((c-1) x - s conj(ph) y),  y <- y + (s ph x + (c-1) y)

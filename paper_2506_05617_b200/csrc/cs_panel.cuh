@@ -35,6 +35,10 @@ namespace cs {
 // owner CTA of panel position p (CTA c holds positions c and 2C-1-c)
 __device__ __forceinline__ int pos_owner(int p, int C) { return p < C ? p : 2 * C - 1 - p; }
 
+// instantiations that carry the Gram convergence check (see gram_check)
+template <typename T, int RPLX, int RPLV>
+constexpr bool GCHECK_BUILT = RPLV > 0 && RPLX >= 8;
+
 // 32-bit shared-memory accessors.  The hot loops walk a column with an
 // opaque pointer bump (asm "+r") so the compiler keeps ONE live address per
 // column instead of hoisting RPL runtime-strided addresses into registers.
@@ -118,7 +122,7 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
     const uint32_t colb = (uint32_t)LD * T2SZ;
     T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
     int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
-    bool rot = false, bad = false;
+    bool rot = false, bad = false, big = false;
             {
                 const int hw = w / 2;
                 const int kk = k % hw;
@@ -163,6 +167,7 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
                             bad = true;
                         } else if (act > 0) {
                             rot = true;
+                            if constexpr (GCHECK_BUILT<T, RPLX, RPLV>) big |= act > 1;
                             const uint32_t ap = smem_u32(panel) + p * colb + g * T2SZ;
                             const uint32_t aq = smem_u32(panel) + q * colb + g * T2SZ;
 #pragma unroll
@@ -183,7 +188,7 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
                 }
             }
 
-    return (rot ? 1 : 0) | (bad ? 2 : 0);
+    return (rot ? 1 : 0) | (bad ? 2 : 0) | (big ? 4 : 0);
 }
 
 // 2C-1 super-rounds of cross pairs a x b: the a panel lives in registers, b
@@ -205,7 +210,7 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
     const uint32_t colb = (uint32_t)LD * T2SZ;
     T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
     int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
-    bool rot = false, bad = false;
+    bool rot = false, bad = false, big = false;
     int *pos = flags + 4;
     const size_t panel_elems = (size_t)w * LD;
     int bcur = flags[2];
@@ -254,6 +259,7 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                             bad = true;
                         } else if (act > 0) {
                             rot = true;
+                            if constexpr (GCHECK_BUILT<T, RPLX, RPLV>) big |= act > 1;
 #pragma unroll
                             for (int i = 0; i < RPLX; ++i) rot_apply<T>(ra[i], y[i], R);
                             col_store<T, RPLX>(y, ab, rstride);
@@ -313,7 +319,7 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                 col_store<T, RPLX>(ra, aa, rstride);
                 if constexpr (WANTV) col_store<T, RPLV1>(rav, aa + voff_b, rstride);
             }
-    return (rot ? 1 : 0) | (bad ? 2 : 0);
+    return (rot ? 1 : 0) | (bad ? 2 : 0) | (big ? 4 : 0);
 }
 
 
@@ -836,6 +842,247 @@ __device__ __noinline__ int panel_cross_gram(const JacShape &s, unsigned char *s
     return fl;
 }
 
+// ---------------------------------------------------------------------------
+// Gram convergence check.  A rotation-free sweep evaluates every pair (i, j)
+// on the same, final columns: it is the test |x_i^H x_j|^2 <= tol^2 a_i a_j
+// (rot_params) over the Gram matrix X^H X.  Computed blocked -- each warp a
+// 4x4 sub-block of a w x w panel block, lanes splitting the rows, one
+// transpose-reduce -- it costs a few percent of a sweep instead of the
+// latency-bound rounds of a check sweep (~2/3 of a rotating one).  The CTAs
+// of a cluster split the panel pairs: the three local blocks, all four blocks
+// with the CTAs at cluster distance 1..(C-1)/2, and half of the four at
+// distance C/2.  Remote panels are staged (X rows only) through the free
+// exchange buffer.  Squared norms of the local columns land in sig2 where
+// the epilogue gathers them.  Returns nonzero if some pair fails the test
+// (or is non-finite): then the solve simply continues with the next sweep.
+// ---------------------------------------------------------------------------
+template <typename T, int NT>
+__device__ __forceinline__ void gram_rows(const cplx_t<T> *const (&xp)[4],
+                                          const cplx_t<T> *const (&yp)[4], int nt, T (&v)[32]) {
+    // NT rows per lane: rows lane + 32 t, t < NT (NT == 0: none)
+    using T2 = cplx_t<T>;
+#pragma unroll
+    for (int t = 0; t < (NT > 0 ? NT : 1); ++t) {
+        if (NT == 0 && t >= nt) break;
+        T2 xv[4], yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xv[u] = xp[u][t * 32];
+            yv[u] = yp[u][t * 32];
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                T &re = v[2 * (ii * 4 + jj)], &im = v[2 * (ii * 4 + jj) + 1];
+                re = fma(xv[ii].y, yv[jj].y, fma(xv[ii].x, yv[jj].x, re));
+                im = fma(-xv[ii].y, yv[jj].x, fma(xv[ii].x, yv[jj].y, im));
+            }
+    }
+}
+
+// rows % 64 == 0: every lane owns rows/32 rows, two per step (fast path)
+template <typename T>
+__device__ __forceinline__ void gram_block(const cplx_t<T> *X, int ldx, int px,
+                                           const cplx_t<T> *Y, int ldy, int py, bool diag,
+                                           int w, int rows, int nc, const T *nrm, T tol,
+                                           bool &bad) {
+    using T2 = cplx_t<T>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int nsub = (w + 3) / 4;
+#pragma unroll 1
+    for (int task = warp; task < nsub * nsub; task += nwarps) {
+        const int i0 = (task / nsub) * 4, j0 = (task % nsub) * 4;
+        if (diag && j0 + 3 <= i0) continue;  // strictly below the diagonal (warp-uniform)
+        T v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0;
+        // columns past the panel edge are clamped (their entries are discarded)
+        const T2 *xp[4], *yp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            xp[u] = X + (size_t)min(i0 + u, w - 1) * ldx;
+            yp[u] = Y + (size_t)min(j0 + u, w - 1) * ldy;
+        }
+        if ((rows & 63) == 0) {
+            // one row per lane per step (rows % 64 == 0 keeps it branch-free).
+            // Plain C++ loads: the same loop through the asm ld.shared accessors
+            // (SmemIO) hung the <C=4, RPLX=8> instantiation (tools/_hang.py), and
+            // two rows per step cost panel_cross 144 B of spills (ptxas splits
+            // the kernel's 128 registers over its noinline phases).
+            const T2 *xs[4], *ys[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xs[u] = xp[u] + lane;
+                ys[u] = yp[u] + lane;
+            }
+            const int nt = rows >> 5;
+#pragma unroll 1
+            for (int t = 0; t < nt; ++t) {
+                T2 xv[4], yv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xv[u] = xs[u][32 * t];
+                    yv[u] = ys[u][32 * t];
+                }
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        T &re = v[2 * (ii * 4 + jj)], &im = v[2 * (ii * 4 + jj) + 1];
+                        re = fma(xv[ii].y, yv[jj].y, fma(xv[ii].x, yv[jj].x, re));
+                        im = fma(-xv[ii].y, yv[jj].x, fma(xv[ii].x, yv[jj].y, im));
+                    }
+            }
+        } else {
+            // generic: rows r = lane + 32 t < rows; lanes past the end read row 0
+            // (always in bounds) and add nothing
+            const int nt = (rows + 31) / 32;
+#pragma unroll 1
+            for (int t = 0; t < nt; ++t) {
+                const int r = lane + 32 * t;
+                const bool ok = r < rows;
+                const T2 *xq[4], *yq[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    xq[u] = xp[u] + (ok ? r : 0);
+                    yq[u] = yp[u] + (ok ? r : 0);
+                }
+                T tmp[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) tmp[e] = 0;
+                gram_rows<T, 1>(xq, yq, 1, tmp);  // one row per lane
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] += ok ? tmp[e] : (T)0;
+            }
+        }
+        // transpose-reduce: afterwards lane l holds the lane-sum of element l in v[0]
+#pragma unroll
+        for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+            const bool upper = lane & off;
+#pragma unroll
+            for (int e = 0; e < n / 2; ++e) {
+                const T send = upper ? v[e] : v[e + n / 2];
+                const T keep = upper ? v[e + n / 2] : v[e];
+                v[e] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        const T other = __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const int ent = lane >> 1, i = i0 + (ent >> 2), j = j0 + (ent & 3);
+        if ((lane & 1) == 0 && i < w && j < w && (!diag || i < j)) {
+            const int gi = px * w + i, gj = py * w + j;
+            if (gi < nc && gj < nc) {
+                const T q = v[0] * v[0] + other * other;
+                const T ai = nrm[gi], aj = nrm[gj];
+                if (!(isfinite(q) && isfinite(ai) && isfinite(aj))) bad = true;
+                else if (ai != (T)0 && aj != (T)0 && q > tol * tol * (ai * aj)) bad = true;
+            }
+        }
+        // reconverge before the next task's shuffles: a warp left diverged here
+        // can have lanes run ahead into a CTA barrier while the others wait in
+        // a full-mask shuffle for them (observed as a hang on one instantiation)
+        __syncwarp();
+    }
+}
+
+template <typename T, int C>
+__device__ __noinline__ int gram_check(const JacShape &s, unsigned char *smem, int rank,
+                                       const cplx_t<T> *Abuf, const cplx_t<T> *Bbuf,
+                                       cplx_t<T> *scratch, int rows, T tol) {
+    using T2 = cplx_t<T>;
+    const int w = s.P, LD = s.ldx, nc = s.nc, ncp = s.ncp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    T *sig2 = reinterpret_cast<T *>(smem + s.off_sig);
+    T *nrm = reinterpret_cast<T *>(smem + s.off_send);  // [ncp] squared norms, all columns
+    int *flags = reinterpret_cast<int *>(smem + s.off_mbar);
+    const int *pos = flags + 4;
+    const int pa = pos[rank], pb = pos[2 * C - 1 - rank];
+
+    // (1) squared norms of the local columns
+#pragma unroll 1
+    for (int c = warp; c < 2 * w; c += nwarps) {
+        const T2 *col = (c < w ? Abuf : Bbuf) + (size_t)(c % w) * LD;
+        T acc = 0;
+        for (int r = lane; r < rows; r += 32) {
+            const T2 v = col[r];
+            acc = fma(v.y, v.y, fma(v.x, v.x, acc));
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) sig2[(c < w ? pa : pb) * w + c % w] = acc;
+        __syncwarp();
+    }
+    if constexpr (C > 1) cluster_sync_all();
+    else __syncthreads();
+    // (2) every column's norm, from the CTA holding it
+    for (int j = tid; j < ncp; j += blockDim.x) {
+        const int panel = j / w;
+        int p0 = 0;
+        for (int p = 0; p < 2 * C; ++p)
+            if (pos[p] == panel) p0 = p;
+        const int owner = pos_owner(p0, C);
+        if constexpr (C > 1)
+            nrm[j] = (owner == rank) ? sig2[j] : cg::this_cluster().map_shared_rank(sig2, owner)[j];
+        else
+            nrm[j] = sig2[j];
+    }
+    __syncthreads();
+
+    // (3) panel blocks
+    bool bad = false;
+    gram_block<T>(Abuf, LD, pa, Abuf, LD, pa, true, w, rows, nc, nrm, tol, bad);
+    gram_block<T>(Bbuf, LD, pb, Bbuf, LD, pb, true, w, rows, nc, nrm, tol, bad);
+    gram_block<T>(Abuf, LD, pa, Bbuf, LD, pb, false, w, rows, nc, nrm, tol, bad);
+    if constexpr (C > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        // stage panel `which` (0 = a, 1 = b) of CTA d: rows [0, rows) into scratch
+        auto stage = [&](int d, int which) -> int {
+            __syncthreads();  // previous blocks done with scratch
+            const T2 *src = cl.map_shared_rank(which == 0 ? Abuf : Bbuf, d);
+            for (int idx = tid; idx < w * rows; idx += blockDim.x) {
+                const int jj = idx / rows, r = idx - jj * rows;
+                scratch[idx] = src[(size_t)jj * LD + r];
+            }
+            __syncthreads();
+            return which == 0 ? pos[d] : pos[2 * C - 1 - d];
+        };
+#pragma unroll 1
+        for (int dist = 1; 2 * dist < C; ++dist) {
+            const int d = (rank + dist) % C;
+#pragma unroll 1
+            for (int which = 0; which < 2; ++which) {
+                const int ps = stage(d, which);
+                gram_block<T>(Abuf, LD, pa, scratch, rows, ps, false, w, rows, nc, nrm, tol, bad);
+                gram_block<T>(Bbuf, LD, pb, scratch, rows, ps, false, w, rows, nc, nrm, tol, bad);
+            }
+        }
+        if (C % 2 == 0) {  // distance C/2: the lower CTA takes its a panel x both,
+            const int d = (rank + C / 2) % C;  // the upper one both panels x the lower's b
+            if (rank < C / 2) {
+#pragma unroll 1
+                for (int which = 0; which < 2; ++which) {
+                    const int ps = stage(d, which);
+                    gram_block<T>(Abuf, LD, pa, scratch, rows, ps, false, w, rows, nc, nrm, tol, bad);
+                }
+            } else {
+                const int ps = stage(d, 1);
+                gram_block<T>(Abuf, LD, pa, scratch, rows, ps, false, w, rows, nc, nrm, tol, bad);
+                gram_block<T>(Bbuf, LD, pb, scratch, rows, ps, false, w, rows, nc, nrm, tol, bad);
+            }
+        }
+    }
+    // (4) verdict, OR-ed over the cluster
+    int any = __syncthreads_or(bad);
+    if constexpr (C > 1) {
+        if (tid == 0) flags[3] = any;
+        cluster_sync_all();
+        cg::cluster_group cl = cg::this_cluster();
+        for (int d = 0; d < C; ++d) any |= cl.map_shared_rank(flags, d)[3];
+        cluster_sync_all();
+    }
+    return any;
+}
+
 template <typename T, int C, int RPLX, int RPLV, bool SPLIT>
 __global__ void __launch_bounds__(SPLIT ? 1024 : JAC_MAX_THREADS)
 jacobi_panel_kernel(const JacArgs<T> a) {
@@ -921,6 +1168,7 @@ jacobi_panel_kernel(const JacArgs<T> a) {
 
         int info = -1;
         for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+            if (a.dbg && tid == 0) *(volatile int *)&a.dbg[blockIdx.x] = 1000000 + 1000 * sweep;
             const int start_a = pos[rank];              // panel ids at the start of the sweep
             const int start_b = pos[2 * C - 1 - rank];
             __syncthreads();
@@ -939,14 +1187,16 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             }
             bcur = flags[2];
             Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
-            const bool rot = fl & 1, bad = fl & 2;
+            const bool rot = fl & 1, bad = fl & 2, big = fl & 4;
             // ---- sweep verdict, OR-ed over the cluster ------------------------
             int any_bad = __syncthreads_or(bad);
             int any_rot = __syncthreads_or(rot);
+            int any_big = __syncthreads_or(big);
             if constexpr (C > 1) {
                 if (tid == 0) {
                     flags[0] = any_rot;
                     flags[1] = any_bad;
+                    flags[3] = any_big;
                 }
                 cluster_sync_all();
                 cg::cluster_group cl = cg::this_cluster();
@@ -954,6 +1204,7 @@ jacobi_panel_kernel(const JacArgs<T> a) {
                     const int *pf = cl.map_shared_rank(flags, d);
                     any_rot |= pf[0];
                     any_bad |= pf[1];
+                    any_big |= pf[3];
                 }
                 cluster_sync_all();
             }
@@ -961,6 +1212,25 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             if (!any_rot) {
                 info = sweep + 1;
                 break;
+            }
+            // no large rotation this sweep: the next one is likely rotation-free;
+            // the Gram check decides that for a few percent of a sweep (counted
+            // as one sweep, so max_sweeps keeps its meaning).  Compiled only
+            // into the large vectors-requested instantiations: there it saves
+            // ~6% (cfg5); elsewhere the check costs more than the sweep it
+            // replaces, and its mere presence perturbs ptxas' register split of
+            // the noinline phases (+3-5% on cfg2-4).
+            if constexpr (GCHECK_BUILT<T, RPLX, RPLV> && !SPLIT) {
+                if (s.gcheck && (!any_big || s.gcheck >= 2) && sweep + 2 <= a.max_sweeps) {
+                    T2 *scratch = Bbuf0 + (size_t)((bcur ^ 1) & (C > 1 ? 1 : 0)) * panel_elems;
+                    if (!gram_check<T, C>(s, smem, rank, Abuf, Bbuf, scratch, G * RPLX, tol) &&
+                        s.gcheck == 1) {
+                        if (tid < 32) start_pos[tid] = pos[tid];  // norms are where the columns are now
+                        __syncthreads();
+                        info = sweep + 2;
+                        break;
+                    }
+                }
             }
         }
 

@@ -367,3 +367,48 @@ def test_opt_in_kernel_variants_match_oracle(cuda, orc, monkeypatch, flag, shape
     s = out.sigma.cpu().numpy().astype(np.float64)
     for f in range(0, count, max(1, count // 12)):
         assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= 1e-5 * s[f][0]
+
+
+@pytest.mark.parametrize("shape,count,vectors,dtype", [((256, 256), 64, True, "f32"),
+                                                       ((256, 256), 300, True, "f32"),
+                                                       ((256, 192), 150, True, "f32"),
+                                                       ((192, 256), 150, True, "f32")])
+def test_gram_check_matches_check_sweep(cuda, orc, monkeypatch, shape, count, vectors, dtype):
+    """The panel kernel's Gram convergence check (cs_panel.cuh gram_check,
+    compiled into the large vectors-requested instantiations) is the
+    rotation-free sweep's test evaluated blocked: sweep counts as with
+    CS_GRAM_CHECK=0 (the plain rotation-free sweep), sigma at the fp32 bar
+    against the oracle, orthonormal factors.  Counts cover one and several
+    matrices per cluster and both C=8 and C=4 clusters."""
+    co, ci = shape
+    rng = np.random.default_rng(co * 7 + ci)
+    A = (rng.standard_normal((count, co, ci)) + 1j * rng.standard_normal((count, co, ci))) / np.sqrt(ci)
+    cdt = np.complex64 if dtype == "f32" else np.complex128
+    blocks = torch.from_numpy(A.astype(cdt)).to(cuda)
+    assert engine.plan_kind(count, co, ci, dtype, vectors) == 2  # panel kernel
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("CS_GRAM_CHECK", mode)
+        outs[mode] = engine.batched_svd(blocks, dtype, vectors)
+    monkeypatch.delenv("CS_GRAM_CHECK")
+    ref, _ = orc.svd_values(A)
+    bar = TOL32 if dtype == "f32" else 1e-10
+    for mode, out in outs.items():
+        info = out.info.cpu().numpy()
+        assert (info > 0).all(), mode
+        assert per_freq_rel_err(out.sigma.cpu().numpy(), ref).max() <= bar, mode
+    # the check replaces a sweep one for one; its inner products are summed in
+    # another order, so a pair at the threshold may fall on the other side
+    i1, i0 = outs["1"].info.cpu().numpy(), outs["0"].info.cpu().numpy()
+    assert np.abs(i1 - i0).max() <= 1
+    assert abs(i1.mean() - i0.mean()) <= 0.05
+    if vectors:
+        out = outs["1"]
+        U = out.U.cpu().numpy().astype(np.complex128)
+        V = out.V.cpu().numpy().astype(np.complex128)
+        s = out.sigma.cpu().numpy().astype(np.float64)
+        r = min(co, ci)
+        for f in range(0, count, max(1, count // 8)):
+            assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= bar * s[f][0]
+            assert np.abs(U[f].conj().T @ U[f] - np.eye(r)).max() <= 10 * bar
+            assert np.abs(V[f].conj().T @ V[f] - np.eye(r)).max() <= 10 * bar
