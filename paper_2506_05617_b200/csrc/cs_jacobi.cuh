@@ -225,7 +225,10 @@ __device__ __forceinline__ void rot_apply(cplx_t<T> &x, cplx_t<T> &y, const Rot<
 // A complex64 value is one register pair; one f32x2 instruction does both of
 // its components, and ptxas folds the component swap (.LO_HI) and a per-lane
 // sign into the operand for free.  Each lane is an IEEE op of its own, so
-// the rounding per component is that of the scalar form.
+// the rounding per component is that of the scalar form.  Opt-in (-DCS_F32X2):
+// same-box A/B on cfg5 (tools/abtime.py) measured cold 12.24 s vs 12.20 s and
+// warm 5.19 s vs 4.99 s for the scalar form -- the cross rounds are latency-,
+// not issue-bound, so halving the FP32 instruction count does not pay.
 typedef unsigned long long f2p;
 __device__ __forceinline__ f2p p2(float a, float b) {
     f2p r;
@@ -257,7 +260,7 @@ __device__ __forceinline__ f2p fadd2(f2p a, f2p b) {
 
 // fp32: the same (c-1)-form update in 8 paired instructions instead of 16:
 //   dx = (c-1) x - conj(w) y,  dy = w x + (c-1) y,  w = s ph = (wr, wi)
-#ifndef CS_NO_F32X2
+#ifdef CS_F32X2
 template <>
 __device__ __forceinline__ void rot_apply<float>(float2 &x, float2 &y, const Rot<float> &R) {
     const f2p X = p2(x), Y = p2(y), C1 = p2(R.cm1, R.cm1);
@@ -277,7 +280,7 @@ __device__ __forceinline__ void rot_apply<float>(float2 &x, float2 &y, const Rot
 template <typename T, int N>
 __device__ __forceinline__ void pair_dots(const cplx_t<T> (&x)[N], const cplx_t<T> (&y)[N], T &al, T &be,
                                           T &gr, T &gi) {
-#ifndef CS_NO_F32X2
+#ifdef CS_F32X2
     constexpr bool PAIRED = sizeof(T) == 4;
 #else
     constexpr bool PAIRED = false;
