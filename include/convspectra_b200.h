@@ -175,6 +175,27 @@ int cs_materialize_vector(const void *factor, int dtype, int rows, int r, int co
 int cs_apply_conv(const void *W, int dtype, int c_out, int c_in, int k_h, int k_w, int n, int m,
                   const void *x, void *y, void *stream);
 
+/* Spectrum post-processing (analysis.py:35-74), float64
+ * device arrays, stream-ordered.
+ *   cs_spectral_summary: stats[4] = max, min, sum, top (top = max if max > 0
+ *     else 1); counts[64] = np.histogram(values, 64, range=(0, top)) exactly;
+ *     edges[65] (optional) = np.linspace(0, top, 65).  n >= 1 (else CS_EINVAL:
+ *     EmptySpectrum).  Replaces spectral_summary (analysis.py:35-53).
+ *   cs_sort_descending_f64: out = values sorted descending (workspace from
+ *     cs_analysis_workspace).
+ *   cs_wasserstein1_sum: *out_sum = sum_i |a_i - b~_i| over the longer
+ *     spectrum, both inputs sorted descending, the shorter resampled at its
+ *     quantile positions as np.interp does; W1 = out_sum / max(La, Lb).
+ *     Replaces wasserstein1 (analysis.py:56-74). */
+size_t cs_analysis_workspace(long long n);
+int cs_spectral_summary(const double *values, long long n, double *stats,
+                        unsigned long long *counts, double *edges, void *workspace,
+                        size_t workspace_bytes, void *stream);
+int cs_sort_descending_f64(const double *in, double *out, long long n, void *workspace,
+                           size_t workspace_bytes, void *stream);
+int cs_wasserstein1_sum(const double *va, long long La, const double *vb, long long Lb,
+                        double *out_sum, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Device microbenchmarks for the roofline denominators: achieved FP32 / FP64
  * FMA rate in flop/s over `ms` milliseconds of a dependent-FMA kernel. */
 double cs_measure_fma_peak(int dtype, int device);

@@ -15,6 +15,9 @@ Restates the reference's host-side glue around the numba kernels:
                             _complete_zero_columns, U/V swap for wide blocks)
 * ``spectrum_values``    <- pipeline.py:61-69 + blocksvd.py:276 (global
                             stable descending sort)
+* ``summary``            <- analysis.py:35-53 (max/min/mean/condition, 64-bin
+                            histogram over [0, top])
+* ``w1``                 <- analysis.py:56-74 (quantile-coupled W1)
 """
 
 from __future__ import annotations
@@ -208,3 +211,31 @@ def spectrum_values(weights, n, m, tol=DEFAULT_TOL, max_sweeps=DEFAULT_MAX_SWEEP
     if fail.any():
         raise RuntimeError(f"oracle: no convergence at frequency {int(np.argmax(fail))}")
     return sort_descending(np.ascontiguousarray(sig).ravel())
+
+
+def summary(values):
+    """analysis.py:35-53: (max, min, count, condition, mean, hist, edges)."""
+    v = np.asarray(values, dtype=np.float64).ravel()
+    if v.size == 0:
+        raise ValueError("empty spectrum")
+    hi, lo = float(v.max()), float(v.min())
+    top = hi if hi > 0 else 1.0
+    hist, edges = np.histogram(v, bins=64, range=(0.0, top))
+    cond = hi / lo if lo > 0 else np.inf
+    return hi, lo, v.size, cond, float(v.mean()), hist, edges
+
+
+def w1(a, b):
+    """analysis.py:56-74: both descending; the shorter resampled at the
+    longer one's quantile positions t = j/(L-1) by linear interpolation."""
+    x = np.sort(np.asarray(a, dtype=np.float64).ravel())[::-1]
+    y = np.sort(np.asarray(b, dtype=np.float64).ravel())[::-1]
+    if x.size == 0 or y.size == 0:
+        raise ValueError("empty spectrum")
+    if x.size < y.size:
+        x, y = y, x
+    if y.size < x.size:
+        pos_long = np.linspace(0.0, 1.0, x.size)
+        pos_short = np.linspace(0.0, 1.0, y.size)
+        y = np.interp(pos_long, pos_short, y[::-1])[::-1]
+    return float(np.abs(x - y).mean())

@@ -21,7 +21,7 @@ LIBPATH = os.path.join(LIBDIR, LIBNAME)
 
 SOURCES = ["cs_api.cu", "cs_symbol.cu", "cs_jacobi.cu", "cs_jacobi_f32.cu", "cs_jacobi_f64.cu",
            "cs_spectrum.cu", "cs_warm.cu",
-           "cs_operator.cu"]
+           "cs_operator.cu", "cs_analysis.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

@@ -56,6 +56,10 @@ _SIGNATURES = {
                                     _vp]),
     "cs_complete_zero_columns": (_i, [_vp, _i, _ll, _i, _i, _vp, _vp, _vp]),
     "cs_first_failure": (_i, [_vp, _ll, _vp, _vp]),
+    "cs_analysis_workspace": (_sz, [_ll]),
+    "cs_spectral_summary": (_i, [_vp, _ll, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "cs_sort_descending_f64": (_i, [_vp, _vp, _ll, _vp, _sz, _vp]),
+    "cs_wasserstein1_sum": (_i, [_vp, _ll, _vp, _ll, _vp, _vp, _sz, _vp]),
     "cs_spectrum_values_workspace": (_sz, [_ll, _i]),
     "cs_spectrum_values": (_i, [_vp, _i, _ll, _i, _i, _i, _i, _vp, _vp, _sz, _vp]),
     "cs_materialize_vector": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp]),

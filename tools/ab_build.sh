@@ -17,7 +17,7 @@ if [ -n "$REV" ]; then
 fi
 NV=/usr/local/cuda/bin/nvcc
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $CS_AB_FLAGS"
-for f in cs_api cs_symbol cs_jacobi cs_jacobi_f32 cs_jacobi_f64 cs_spectrum cs_warm cs_operator; do
+for f in $(cd "$T/pkg/csrc" && ls *.cu | sed "s/\.cu$//"); do
   $NV $FL -c "$T/pkg/csrc/$f.cu" -o "$T/obj/$f.o" &
 done
 wait
