@@ -196,6 +196,21 @@ int cs_sort_descending_f64(const double *in, double *out, long long n, void *wor
 int cs_wasserstein1_sum(const double *va, long long La, const double *vb, long long Lb,
                         double *out_sum, void *workspace, size_t workspace_bytes, void *stream);
 
+/* FFT route to the symbol field (fft.py:103-151), the
+ * paper's comparison baseline for K1:
+ *   cs_fft_transform: emb (c_out*c_in, m, n) complex of dtype <- taps of each
+ *     channel pair embedded at their wrapped torus offsets (collisions summed
+ *     in tap order), then one forward 2D DFT per pair (cuFFT, exp(-2 pi i ..)).
+ *     emb_bytes >= cs_fft_field_workspace(...).  Replaces fft.py:133-139.
+ *   cs_fft_gather: out (F_u or n*m, c_out, c_in) <- coefficient
+ *     (-j mod m, -i mod n) for block (i, j), representatives when half_grid=1
+ *     (the layout of cs_symbol_field).  Replaces fft.py:141-146. */
+size_t cs_fft_field_workspace(int dtype, int c_out, int c_in, int n, int m);
+int cs_fft_transform(const void *W, int dtype, int c_out, int c_in, int k_h, int k_w, int n, int m,
+                     void *emb, size_t emb_bytes, void *stream);
+int cs_fft_gather(const void *emb, int dtype, int c_out, int c_in, int n, int m, int half_grid,
+                  void *out, void *stream);
+
 /* Device microbenchmarks for the roofline denominators: achieved FP32 / FP64
  * FMA rate in flop/s over `ms` milliseconds of a dependent-FMA kernel. */
 double cs_measure_fma_peak(int dtype, int device);

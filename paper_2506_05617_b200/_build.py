@@ -21,7 +21,9 @@ LIBPATH = os.path.join(LIBDIR, LIBNAME)
 
 SOURCES = ["cs_api.cu", "cs_symbol.cu", "cs_jacobi.cu", "cs_jacobi_f32.cu", "cs_jacobi_f64.cu",
            "cs_spectrum.cu", "cs_warm.cu",
-           "cs_operator.cu", "cs_analysis.cu"]
+           "cs_operator.cu", "cs_analysis.cu", "cs_fft.cu"]
+# cuFFT (the FFT comparison route only) from the CUDA toolkit of this image
+LINK_LIBS = ["-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
@@ -68,7 +70,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIBPATH, objs):
-        run([cc] + ARCH + ["-shared", "-cudart", "static", "-o", LIBPATH] + objs)
+        run([cc] + ARCH + ["-shared", "-cudart", "static", "-o", LIBPATH] + objs + LINK_LIBS)
     return LIBPATH
 
 

@@ -56,6 +56,9 @@ _SIGNATURES = {
                                     _vp]),
     "cs_complete_zero_columns": (_i, [_vp, _i, _ll, _i, _i, _vp, _vp, _vp]),
     "cs_first_failure": (_i, [_vp, _ll, _vp, _vp]),
+    "cs_fft_field_workspace": (_sz, [_i, _i, _i, _i, _i]),
+    "cs_fft_transform": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp, _sz, _vp]),
+    "cs_fft_gather": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     "cs_analysis_workspace": (_sz, [_ll]),
     "cs_spectral_summary": (_i, [_vp, _ll, _vp, _vp, _vp, _vp, _sz, _vp]),
     "cs_sort_descending_f64": (_i, [_vp, _vp, _ll, _vp, _sz, _vp]),

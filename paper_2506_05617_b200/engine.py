@@ -177,6 +177,29 @@ def symbol_field(w_dev, dims_n: int, dims_m: int, dtype: str, half: bool = True,
     return out
 
 
+def fft_symbol_field(w_dev, dims_n: int, dims_m: int, dtype: str, half: bool = True,
+                     timer=None, out=None):
+    """Symbol blocks by the FFT route (cs_fft_transform + cs_fft_gather):
+    embed, batched 2D DFT per channel pair, gather.  ``timer`` gets a mark
+    "tf" between the transform and the gather (s_transform | s_copy)."""
+    co, ci, kh, kw = w_dev.shape
+    total = half_grid_count(dims_n, dims_m) if half else dims_n * dims_m
+    lib = _lib.load()
+    nbytes = lib.cs_fft_field_workspace(dtype_code(dtype), co, ci, dims_n, dims_m)
+    emb = torch.empty(int(nbytes), dtype=torch.uint8, device=w_dev.device)
+    st = stream_ptr(w_dev.device)
+    _lib.check(lib.cs_fft_transform(ptr(w_dev), dtype_code(dtype), co, ci, kh, kw, dims_n, dims_m,
+                                    ptr(emb), nbytes, st), "cs_fft_transform")
+    if timer:
+        timer.mark("tf")
+    if out is None:
+        out = torch.empty((total, co, ci), dtype=complex_dtype(dtype), device=w_dev.device)
+    _lib.check(lib.cs_fft_gather(ptr(emb), dtype_code(dtype), co, ci, dims_n, dims_m, int(half),
+                                 ptr(out), st), "cs_fft_gather")
+    del emb  # stream-ordered reuse by the caching allocator
+    return out
+
+
 def symbol_at_freqs(w_dev, freqs: np.ndarray, dtype: str):
     co, ci, kh, kw = w_dev.shape
     fr = torch.from_numpy(np.ascontiguousarray(freqs, dtype=np.float64)).to(w_dev.device)

@@ -45,7 +45,7 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
                tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
                u0: int = 0, count: int | None = None, assemble: bool = True,
                timer: engine.Timer | None = None, field_out=None,
-               warm_start=None) -> DeviceSpectrum:
+               warm_start=None, method: str = "lfa") -> DeviceSpectrum:
     """K1 -> K2/K3 -> assembly on the current stream, no host synchronisation.
 
     ``warm_start`` (default: when vectors are requested and the panel kernel
@@ -56,8 +56,13 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
         count = total - u0
     if timer:
         timer.mark("t0")
-    fld = engine.symbol_field(w_dev, n, m, dtype, half=True, f_first=u0, f_count=count,
-                              out=field_out)
+    if method == "fft":  # fft.py route to the same representative blocks
+        if u0 != 0 or count != total:
+            raise ValueError("the FFT route builds the whole half grid (u0=0, count=None)")
+        fld = engine.fft_symbol_field(w_dev, n, m, dtype, half=True, timer=timer, out=field_out)
+    else:
+        fld = engine.symbol_field(w_dev, n, m, dtype, half=True, f_first=u0, f_count=count,
+                                  out=field_out)
     if timer:
         timer.mark("t1")
     co, ci = w_dev.shape[0], w_dev.shape[1]
@@ -162,9 +167,9 @@ def compute_spectrum(kernel: ConvKernel, dims: SpatialDims, method: str = "lfa",
         raise ValueError(f"unknown boundary {boundary!r}")
     if boundary == DIRICHLET and method != "explicit":
         raise ValueError(f"method {method!r} only supports periodic boundaries")
-    if method != "lfa":
+    if method == "explicit":
         raise NotImplementedError(
-            f"method {method!r} is outside the B200 hot path (only 'lfa' is implemented)")
+            "method 'explicit' (the dense oracle, explicit.py) is outside the B200 hot path")
     if layout not in LAYOUTS:
         raise ValueError(f"unknown layout {layout!r}")
     resolve_workers(workers)
@@ -173,19 +178,25 @@ def compute_spectrum(kernel: ConvKernel, dims: SpatialDims, method: str = "lfa",
     dt = _resolve_dtype(kernel, dtype)
     n, m = dims.n, dims.m
     co, ci = kernel.c_out, kernel.c_in
-    engine.check_budget(field_bytes((co, ci), n, m, dt, not values_only),
-                        engine.device_budget_bytes(dev, mem_budget_gib),
-                        f"LFA solve ({engine.half_grid_count(n, m)} blocks of {co}x{ci})")
+    need = field_bytes((co, ci), n, m, dt, not values_only)
+    if method == "fft":  # plus the embedded channel-pair grids (fft.py:123-130)
+        need += co * ci * n * m * (8 if dt == "f32" else 16)
+    engine.check_budget(need, engine.device_budget_bytes(dev, mem_budget_gib),
+                        f"{method.upper()} solve ({engine.half_grid_count(n, m)} blocks of {co}x{ci})")
     w = engine.weights_to_device(kernel, dt, dev)
     tm = engine.Timer(dev)
-    res = lfa_device(w, n, m, dt, not values_only, tol, max_sweeps, timer=tm)
+    res = lfa_device(w, n, m, dt, not values_only, tol, max_sweeps, timer=tm, method=method)
     f = engine.first_failure(res.info)
     if f >= 0:
         reps = engine.half_grid_indices(n, m)
         from .kernels import FrequencyGrid
         engine.raise_convergence(int(reps[f]), FrequencyGrid(dims).frequencies, max_sweeps)
-    timings = PhaseTimings.build(tm.seconds("t0", "t1"), tm.seconds("t1", "t3"), 0.0)
+    if method == "fft":  # s_transform = embed + DFT, s_copy = gather (fft.py:139-146)
+        timings = PhaseTimings.build(tm.seconds("t0", "tf"), tm.seconds("t1", "t3"),
+                                     tm.seconds("tf", "t1"))
+    else:
+        timings = PhaseTimings.build(tm.seconds("t0", "t1"), tm.seconds("t1", "t3"), 0.0)
     values = res.values.cpu().numpy()
-    return SpectrumResult(values=values, method="lfa", boundary=PERIODIC, dims=dims,
+    return SpectrumResult(values=values, method=method, boundary=PERIODIC, dims=dims,
                           channels=(ci, co), timings=timings,
                           device_values=res.values if return_device_tensors else None)

@@ -161,7 +161,7 @@ def test_method_and_boundary_validation():
     with pytest.raises(ValueError):
         cs.compute_spectrum(k, d, boundary="dirichlet")
     with pytest.raises(NotImplementedError):
-        cs.compute_spectrum(k, d, method="fft")
+        cs.compute_spectrum(k, d, method="explicit")
 
 
 def test_no_cpu_fallback_without_cuda():

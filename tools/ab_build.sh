@@ -21,5 +21,5 @@ for f in $(cd "$T/pkg/csrc" && ls *.cu | sed "s/\.cu$//"); do
   $NV $FL -c "$T/pkg/csrc/$f.cu" -o "$T/obj/$f.o" &
 done
 wait
-$NV -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$ROOT/ab_libs/lib$NAME.so" "$T"/obj/*.o
+$NV -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$ROOT/ab_libs/lib$NAME.so" "$T"/obj/*.o -lcufft -Xlinker -rpath,/usr/local/cuda/lib64
 echo "built ab_libs/lib$NAME.so"
