@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the FFT-route / analysis timings")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the cpu_baseline / reference sample")
     return ap.parse_args()
@@ -386,6 +387,41 @@ def run_ours(args, wl, rank, world, local_rank):
                        if len(layers) > 1 else
                        f"paper_2506_05617_b200.compute_spectrum(kernel, dims, values_only={not wl.vectors})")}
 
+    # SURVEY 8(f) rows measured next to the hot path (1 GPU, single layer):
+    # the FFT route's assembly (the paper's comparison baseline) vs K1, and
+    # the device post-processing of the spectrum this step produced
+    extras = None
+    if world == 1 and len(layers) == 1 and not args.no_extras:
+        l, w = layers[0], w_dev[0]
+        vals = outs[0].values
+        del outs
+        torch.cuda.empty_cache()
+        tf = engine.Timer(dev)
+        for rep in range(2):  # second repetition timed (cuFFT plan warm)
+            tf = engine.Timer(dev)
+            tf.mark("t0")
+            fld = engine.fft_symbol_field(w, l.n, l.m, dt, half=True, timer=tf)
+            tf.mark("t1")
+            del fld
+        k1_ms = phases["assembly_K1_ms"]
+        fft_ms = 1e3 * tf.seconds("t0", "t1")
+        ta = engine.Timer(dev)
+        ta.mark("a0")
+        summ = cs.spectral_summary(vals)
+        ta.mark("a1")
+        w1 = cs.wasserstein1(vals, vals[::2])
+        ta.mark("a2")
+        extras = {
+            "fft_route_assembly_ms": {"transform": 1e3 * tf.seconds("t0", "tf"),
+                                      "gather": 1e3 * tf.seconds("tf", "t1"), "total": fft_ms,
+                                      "k1_ms": k1_ms, "k1_speedup": fft_ms / k1_ms,
+                                      "what": "embed + batched cuFFT C2C (c_out*c_in 2D DFTs) + "
+                                              "gather to the same representative blocks as K1"},
+            "analysis_ms": {"spectral_summary": 1e3 * ta.seconds("a0", "a1"),
+                            "wasserstein1_vs_half": 1e3 * ta.seconds("a1", "a2"),
+                            "values": int(vals.numel()), "sigma_max": summ.sigma_max, "w1": w1},
+        }
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, host_threads(), args.cpu_seconds)
@@ -420,7 +456,7 @@ def run_ours(args, wl, rank, world, local_rank):
             "config": workload_config(wl, world),
             "roofline": roofline, "roofline_assembly": roofline_k1,
             "phases": phases, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "sweeps_mean": sweeps_mean, "converged": ok,
+            "clocks": clocks, "sweeps_mean": sweeps_mean, "converged": ok, "extras": extras,
             "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)
