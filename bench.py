@@ -340,12 +340,27 @@ def run_ours(args, wl, rank, world, local_rank):
                                    "dependent-FFMA probe); MEASURED_PEAKS.json holds no FP32 peak",
                     "algorithmic": "Golub-Reinsch sigma+U+V count x4 complex per unique block "
                                    "(SURVEY 8(d)); Jacobi executes ~3.5x more"}
+        # DRAM traffic per step from the committed ncu capture of this workload
+        # (profiles/r01d_traffic_cfg5.json; null for other workloads / N > 1)
+        trf = {}
+        tpath = os.path.join(ROOT, "profiles", "r01d_traffic_cfg5.json")
+        if world == 1 and os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            if tj.get("workload") == workload_config(wl, world).get("workload"):
+                trf = tj["per_step"]
+        if "jacobi_panel_kernel" in trf:
+            j = trf["jacobi_panel_kernel"]
+            roofline["traffic"] = (j["dram_read_GB"] + j["dram_write_GB"]) * 1e9
+            roofline["traffic_source"] = "ncu dram__bytes_read+write per step, profiles/r01d_traffic_cfg5.json"
         asm_b = sum(asm_bytes(l, c) for l, c in zip(layers, shares))
         hbm = peaks.get("hbm_gbs", 6650.0)
         k1_s = sum(k1) / args.steps
         roofline_k1 = {"kernel": "symbol_rows_kernel (K1 half-grid assembly)", "bound": "hbm",
                        "achieved": asm_b / k1_s / 1e9, "peak": hbm, "unit": "GB/s",
-                       "frac": asm_b / k1_s / 1e9 / hbm, "traffic": None,
+                       "frac": asm_b / k1_s / 1e9 / hbm,
+                       "traffic": ((trf["symbol_rows_kernel"]["dram_read_GB"] +
+                                    trf["symbol_rows_kernel"]["dram_write_GB"]) * 1e9
+                                   if "symbol_rows_kernel" in trf else None),
                        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
 
     # e2e through the public API: host weights -> compute_spectrum(values_only=False)
