@@ -91,3 +91,18 @@ int jacobi_dispatch_f32(const JacArgs<float> &a, bool wantv, cudaStream_t st, bo
 }
 
 }  // namespace cs
+
+#ifdef CS_PHASE_CLOCKS
+// experiment builds only: per-phase cycle totals of the f32 panel kernels
+// [0] Gram G=P^H P, [1] rotations on G, [2] P += P D, [3] within rounds,
+// [4] scalar cross phase (tools/gram_split.py)
+extern "C" int cs_debug_phase_cycles(unsigned long long *out, int reset) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    cudaMemcpyFromSymbol(out, cs::g_phase_cycles, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(cs::g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

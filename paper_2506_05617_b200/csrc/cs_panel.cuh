@@ -32,6 +32,11 @@
 
 namespace cs {
 
+#ifdef CS_PHASE_CLOCKS
+// experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_PHASE_CLOCKS)
+static __device__ unsigned long long g_phase_cycles[8];
+#endif
+
 // owner CTA of panel position p (CTA c holds positions c and 2C-1-c)
 __device__ __forceinline__ int pos_owner(int p, int C) { return p < C ? p : 2 * C - 1 - p; }
 
@@ -922,14 +927,31 @@ __device__ __noinline__ int panel_cross_gram(const JacShape &s, unsigned char *s
     T2 *Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
 #pragma unroll 1
     for (int t = 0; t < 2 * C - 1; ++t) {
+#ifdef CS_PHASE_CLOCKS
+        long long c0 = clock64();
+#endif
         gram_phase<T>(smem, smem_u32(Abuf), smem_u32(Bbuf), w, LD, mr, Gm, Dm);
         __syncthreads();
+#ifdef CS_PHASE_CLOCKS
+        long long c1 = clock64();
+#endif
         const int f = inner_phase<T>(w, Gm, Dm, prm, tol);
         fl |= f;
+#ifdef CS_PHASE_CLOCKS
+        long long c2 = clock64();
+#endif
         if (__syncthreads_or(f & 1)) {
             update_phase<T, 16>(smem_u32(Abuf), smem_u32(Bbuf), LD, mr, nvr, VOFF, Dm);
         }
         __syncthreads();
+#ifdef CS_PHASE_CLOCKS
+        if (threadIdx.x == 0) {  // per-phase cycle totals (tools/gram_split.py)
+            long long c3 = clock64();
+            atomicAdd(&g_phase_cycles[0], (unsigned long long)(c1 - c0));
+            atomicAdd(&g_phase_cycles[1], (unsigned long long)(c2 - c1));
+            atomicAdd(&g_phase_cycles[2], (unsigned long long)(c3 - c2));
+        }
+#endif
         if constexpr (C > 1) {
             if (t == 2 * C - 2) break;
             // panel rotation; the new a panel is staged through registers because
@@ -1352,8 +1374,20 @@ jacobi_panel_kernel(const JacArgs<T> a) {
                                   Bbuf0 + (size_t)(flags[2] ^ 1) * panel_elems, vw, nc);
                 fl |= panel_cross<T, C, RPLX, RPLV, true>(s, smem, rank, Abuf, Bbuf0, tol, vw);
             } else {
+#ifdef CS_PHASE_CLOCKS
+                long long c0 = clock64();
+#endif
                 fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
+#ifdef CS_PHASE_CLOCKS
+                long long c1 = clock64();
+#endif
                 fl |= panel_cross<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
+#ifdef CS_PHASE_CLOCKS
+                if (tid == 0) {
+                    atomicAdd(&g_phase_cycles[3], (unsigned long long)(c1 - c0));
+                    atomicAdd(&g_phase_cycles[4], (unsigned long long)(clock64() - c1));
+                }
+#endif
             }
             bcur = flags[2];
             Bbuf = Bbuf0 + (size_t)bcur * panel_elems;

@@ -88,3 +88,19 @@ def test_fft_budget_and_explicit_refused(cuda):
         cs.fft_symbol_field(cs.random_kernel(64, 64, 3, 3), cs.SpatialDims(64, 64), mem_budget_gib=0.01)
     with pytest.raises(NotImplementedError):
         cs.compute_spectrum(cs.random_kernel(2, 2, 3, 3), cs.SpatialDims(4, 4), method="explicit")
+
+
+def test_fft_route_cfg5_field_matches_k1(cuda):
+    """Full-size FFT route (cfg5: 65536 channel pairs x 2^16-point DFTs, 2^32
+    points, 64-bit cuFFT plan) against K1 on every representative block."""
+    layer = configs.WORKLOADS[5].layers[0]
+    w = torch.from_numpy(configs.layer_weights(layer)).to(cuda)
+    a = engine.fft_symbol_field(w, layer.n, layer.m, "f32", half=True)
+    b = engine.symbol_field(w, layer.n, layer.m, "f32", half=True)
+    assert a.shape == b.shape == (engine.half_grid_count(layer.n, layer.m), 256, 256)
+    worst = 0.0
+    for s in range(0, a.shape[0], 4096):  # chunked: the difference of 17 GB fields
+        d = (a[s:s + 4096] - b[s:s + 4096]).abs().amax(dim=(1, 2))
+        ref = b[s:s + 4096].abs().amax(dim=(1, 2))
+        worst = max(worst, (d / ref).max().item())
+    assert worst <= 2e-6
