@@ -122,28 +122,14 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     s.Rv = wantv ? s.nc : 0;
     int G = 1;
     while (G * 2 <= 32 && w * G * 2 <= JAC_MAX_THREADS && G * 2 * 4 <= pow2ceil(s.mr)) G *= 2;
-    // deferred V (cs_panel.cuh "DV"): vectors, fp32, clusters, panel pairs of
-    // 2w = 32 columns, 2w Q rows instead of nc V rows.  Opt-in (CS_DV=1):
-    // correct, but slower on cfg5 (warm 5.71 s with 32 lanes per slot, 5.38-5.74 s
-    // with 16 lanes and two CTAs per SM, vs 4.92 s in-panel): the GEMM does the
-    // rotation's flops again for every super-round with any rotation, plus the
-    // Q rows -- kept as the tested skeleton of a tensor-core back-transformation.
-    const char *dvenv = std::getenv("CS_DV");
-    s.dv = (wantv && sizeof(T) == 4 && C >= 2 && 2 * w == 32 && s.mr >= 128 && s.mr <= 256 &&
-            dvenv && dvenv[0] == '1') ? 1 : 0;
-    if (s.dv) {
-        const char *dg = std::getenv("CS_DV_G");  // experiment: 16 (2 CTAs/SM) or 32 lanes per slot
-        G = (dg && std::atoi(dg) == 16) ? 16 : 32;
-        s.Rv = 2 * w;
-    }
     const int rplx = std::max(2, pow2ceil((s.mr + G - 1) / G));
-    const int rplv = s.dv ? 2 * w / G : (wantv ? rplx : 0);
+    const int rplv = wantv ? rplx : 0;
     const int budget = sizeof(T) == 4 ? 16 : 8;  // complex rows per column held in registers
     // with vectors, X and V rows go to separate warps when 2x the threads fit
     // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
-    s.split = (!s.dv && wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&
+    s.split = (wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&
                rplx <= budget / 2 && std::getenv("CS_SPLIT") != nullptr) ? 1 : 0;  // opt-in: spills at 64 regs
-    if (s.dv ? rplx > budget : (!s.split && rplx + rplv > budget)) return false;
+    if (!s.split && rplx + rplv > budget) return false;
     s.G = G;
     s.RPL = rplx;
     s.threads = s.split ? 2 * w * G : ((w * G + 31) / 32) * 32;
@@ -159,14 +145,14 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     // Gram-blocked cross phase (opt-in CS_GRAM=1: correct, but 2.8x slower than the
     // scalar cross rounds on cfg5 in SIMT; kept as the skeleton for a tensor-core version)
     const char *genv = std::getenv("CS_GRAM");
-    s.gram = (sizeof(T) == 4 && w == 16 && !s.split && !s.dv && genv != nullptr && genv[0] == '1' &&
+    s.gram = (sizeof(T) == 4 && w == 16 && !s.split && genv != nullptr && genv[0] == '1' &&
               w * (s.mr + s.Rv) <= 16 * s.threads) ? 1 : 0;  // a-panel staging: 16 per thread
     const size_t gbytes = s.gram ? 2 * (size_t)(2 * w) * (2 * w + 1) * 2 * sizeof(T) : 0;
     off = align16(off + std::max(s.ncp * sizeof(T), gbytes));
     s.off_recv = off;  // split mode: rotation parameters [2][w]
     off = align16(off + 2 * (size_t)w * 4 * sizeof(T) + 64);
-    s.off_mbar = off;  // sweep flags + panel position tables + per-slot round counters
-    off = align16(off + (4 + 64 + 32) * sizeof(int));
+    s.off_mbar = off;  // sweep flags + panel position tables
+    off = align16(off + (4 + 64) * sizeof(int));
     s.off_x = off;
     const size_t panel = (size_t)w * s.ldx * T2sz;
     off = align16(off + panel);
@@ -175,8 +161,6 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     s.smem = off;
     s.smem_resident = 1;
     s.nbuf = 1;
-    const char *ws = std::getenv("CS_WSYNC");  // default on; "0" = CTA barrier per round
-    s.wsync = (G == 32 && !s.split && !s.gram && !(ws && ws[0] == '0')) ? 1 : 0;
     const char *gc = std::getenv("CS_GRAM_CHECK");  // default on; "0" = rotation-free sweep
     // "2" (timing experiment): check after every rotating sweep, ignore the verdict
     s.gcheck = (!s.split && !s.gram && !(gc && gc[0] == '0')) ? ((gc && gc[0] == '2') ? 2 : 1) : 0;
@@ -269,15 +253,14 @@ static int svd_workspace(long long count, int co, int ci, bool wantv, size_t *by
     *bytes = 0;
     if (count <= 0) return CS_OK;
     if (!plan<T>(co, ci, wantv, count, s)) return fail(CS_EINVAL, "batched SVD: no plan");
-    if (s.smem_resident && !s.dv) return CS_OK;
+    if (s.smem_resident) return CS_OK;
     JacArgs<T> a = {};
     a.count = count;
     a.s = s;
     long long ncl = 0;
     int st = dispatch<T>(a, wantv, 0, true, &ncl);
     if (st) return st;
-    if (s.dv) *bytes = (size_t)ncl * s.nc * s.nc * 2 * sizeof(T);  // V per cluster
-    else *bytes = (size_t)ncl * s.C * s.scratch_per_cta * 2 * sizeof(T);
+    *bytes = (size_t)ncl * s.C * s.scratch_per_cta * 2 * sizeof(T);
     return CS_OK;
 }
 
@@ -310,7 +293,7 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
     // working-orientation factors: for wide blocks X = A^H, so X's U is A's V
     a.Uw = (cplx_t<T> *)(a.s.wide ? V : U);
     a.Vw = (cplx_t<T> *)(a.s.wide ? U : V);
-    if (!a.s.smem_resident || a.s.dv) {
+    if (!a.s.smem_resident) {
         size_t need = 0;
         int stt = svd_workspace<T>(count, co, ci, wantv, &need);
         if (stt) return stt;

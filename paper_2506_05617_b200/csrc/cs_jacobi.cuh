@@ -46,8 +46,6 @@ struct JacShape {
     int split;  // panel kernel: separate X and V warps (2x threads)
     int gram;   // panel kernel: Gram-blocked cross phase
     int gcheck; // panel kernel: Gram convergence check instead of the rotation-free sweep
-    int dv;     // panel kernel: deferred V (Q rows in the panels, V in the workspace)
-    int wsync;  // panel kernel: warp-pair hand-off in the cross rounds (G == 32)
     long long num_clusters;
     size_t scratch_per_cta;  // complex elements, generic global-memory mode
 };
@@ -219,96 +217,6 @@ __device__ __forceinline__ void rot_apply(cplx_t<T> &x, cplx_t<T> &y, const Rot<
     x.y += day;
     y.x += dbx;
     y.y += dby;
-}
-
-// ---- packed fp32 pairs: sm_100a FFMA2 / FMUL2 / FADD2 ----------------------
-// A complex64 value is one register pair; one f32x2 instruction does both of
-// its components, and ptxas folds the component swap (.LO_HI) and a per-lane
-// sign into the operand for free.  Each lane is an IEEE op of its own, so
-// the rounding per component is that of the scalar form.  Opt-in (-DCS_F32X2):
-// same-box A/B on cfg5 (tools/abtime.py) measured cold 12.24 s vs 12.20 s and
-// warm 5.19 s vs 4.99 s for the scalar form -- the cross rounds are latency-,
-// not issue-bound, so halving the FP32 instruction count does not pay.
-typedef unsigned long long f2p;
-__device__ __forceinline__ f2p p2(float a, float b) {
-    f2p r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ f2p p2(float2 v) { return p2(v.x, v.y); }
-__device__ __forceinline__ f2p p2s(float2 v) { return p2(v.y, v.x); }  // swapped components
-__device__ __forceinline__ float2 u2(f2p r) {
-    float2 v;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-    return v;
-}
-__device__ __forceinline__ f2p ffma2(f2p a, f2p b, f2p c) {
-    f2p d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ f2p fmul2(f2p a, f2p b) {
-    f2p d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2p fadd2(f2p a, f2p b) {
-    f2p d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-
-// fp32: the same (c-1)-form update in 8 paired instructions instead of 16:
-//   dx = (c-1) x - conj(w) y,  dy = w x + (c-1) y,  w = s ph = (wr, wi)
-#ifdef CS_F32X2
-template <>
-__device__ __forceinline__ void rot_apply<float>(float2 &x, float2 &y, const Rot<float> &R) {
-    const f2p X = p2(x), Y = p2(y), C1 = p2(R.cm1, R.cm1);
-    f2p tn = fmul2(p2(-R.wr, -R.wr), Y);           // -(wr y)
-    tn = ffma2(p2(-R.wi, R.wi), p2s(y), tn);        // -(wr y.x + wi y.y), -(wr y.y - wi y.x)
-    const f2p dx = ffma2(C1, X, tn);
-    f2p u = fmul2(p2(R.wr, R.wr), X);
-    u = ffma2(p2(-R.wi, R.wi), p2s(x), u);          // w x
-    const f2p dy = ffma2(C1, Y, u);
-    x = u2(fadd2(X, dx));
-    y = u2(fadd2(Y, dy));
-}
-#endif
-
-// (alpha, beta, gamma) partial sums of a column pair over N rows of a lane:
-// alpha += |x|^2, beta += |y|^2, gamma += conj(x) y
-template <typename T, int N>
-__device__ __forceinline__ void pair_dots(const cplx_t<T> (&x)[N], const cplx_t<T> (&y)[N], T &al, T &be,
-                                          T &gr, T &gi) {
-#ifdef CS_F32X2
-    constexpr bool PAIRED = sizeof(T) == 4;
-#else
-    constexpr bool PAIRED = false;
-#endif
-    if constexpr (PAIRED) {
-        f2p A = 0, B = 0, R = 0, I = 0;  // per-component partial sums
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const f2p X = p2(x[i]), Y = p2(y[i]);
-            A = ffma2(X, X, A);
-            B = ffma2(Y, Y, B);
-            R = ffma2(X, Y, R);            // x.x y.x , x.y y.y
-            I = ffma2(X, p2s(y[i]), I);    // x.x y.y , x.y y.x
-        }
-        const float2 a = u2(A), b = u2(B), r = u2(R), im = u2(I);
-        al += a.x + a.y;
-        be += b.x + b.y;
-        gr += r.x + r.y;
-        gi += im.x - im.y;
-    } else {
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            al = fma(x[i].y, x[i].y, fma(x[i].x, x[i].x, al));
-            be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
-            gr = fma(x[i].y, y[i].y, fma(x[i].x, y[i].x, gr));
-            gi = fma(-x[i].y, y[i].x, fma(x[i].x, y[i].y, gi));
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------

@@ -28,10 +28,6 @@ static int fast_c(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry
 
 template <int C_, int RPL_>
 static int panel_rpl(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
-    if constexpr (C_ >= 2 && C_ <= 8 && RPL_ >= 8)
-        if (wantv && a.s.dv)
-            return launch_cluster_kernel<float, C_>(
-                jacobi_panel_kernel<float, C_, RPL_, DV_W2 / (RPL_ == 16 ? 16 : 32), false, true>, a, st, dry, ncl);
     if constexpr (2 * RPL_ <= 16 && true)
         if (wantv && a.s.split)
             return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_, true>, a, st, dry, ncl);

@@ -144,7 +144,13 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
                         const uint32_t aq = smem_u32(panel) + q * colb + g * T2SZ;
                         col_load<T, RPLX>(x, ap, rstride);
                         col_load<T, RPLX>(y, aq, rstride);
-                        pair_dots<T, RPLX>(x, y, al, be, gr, gi);
+#pragma unroll
+                        for (int i = 0; i < RPLX; ++i) {
+                            al = fma(x[i].y, x[i].y, fma(x[i].x, x[i].x, al));
+                            be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                            gr = fma(x[i].y, y[i].y, fma(x[i].x, y[i].x, gr));
+                            gi = fma(-x[i].y, y[i].x, fma(x[i].x, y[i].y, gi));
+                        }
                     }
 #pragma unroll
                     for (int off = 16; off >= 1; off >>= 1) {
@@ -190,133 +196,13 @@ __device__ __noinline__ int panel_within(const JacShape &s, unsigned char *smem,
     return (rot ? 1 : 0) | (bad ? 2 : 0) | (big ? 4 : 0);
 }
 
-
-// ---------------------------------------------------------------------------
-// Deferred V ("DV", vectors requested, fp32, w = 16): the V rows do not live in
-// the panels.  Each panel column carries 2w "Q rows" instead -- the product Q
-// of the rotations of the current phase restricted to the CTA's 2w columns
-// (local index: a-panel column c -> c, b-panel column c -> w + c), reset to
-// the identity when a phase starts.  When the phase ends, V's 2w columns are
-// back-transformed in one batched complex GEMM, V <- V + V (Q - I), with V in
-// a per-cluster global workspace (column-major nc x nc, L2-resident).  The
-// rounds then rotate 2w Q rows instead of nc V rows, the panels shrink to the
-// X rows (two CTAs fit per SM), and the O(nc) V work runs as dense FMA tiles.
-// The rotations, and hence sigma and U, are exactly those of the in-panel V
-// path; V differs only by the rounding of the GEMM (D form: relative to the
-// correction, as rot_apply).
-// ---------------------------------------------------------------------------
-constexpr int DV_W2 = 32;  // 2w: the only panel pair width DV is built for
-
-template <typename T>
-__device__ __forceinline__ void dv_reset_q(cplx_t<T> *Abuf, cplx_t<T> *Bbuf, int w, int LD, int VOFF) {
-    const int n2 = 2 * w;
-    for (int idx = threadIdx.x; idx < n2 * n2; idx += blockDim.x) {
-        const int c = idx / n2, r = idx - c * n2;
-        cplx_t<T> *col = (c < w ? Abuf + (size_t)c * LD : Bbuf + (size_t)(c - w) * LD) + VOFF;
-        col[r] = mk<T>(r == c ? (T)1 : (T)0, (T)0);
-    }
-}
-
-// V[:, cols] += V[:, cols] (Q - I) for the CTA's 2w columns (global ids
-// pa*w + c and pb*w + c); Dm: 2w x 2w staging (row k = input column).  Each
-// thread owns whole rows of V, so reads and writes need no barrier between.
-static __device__ __noinline__ void dv_apply(const float2 *Abuf, const float2 *Bbuf, int pa, int pb, int w,
-                                      int LD, int VOFF, float2 *Dm, float2 *vw, int nc) {
-    constexpr int W2 = DV_W2;
-    for (int idx = threadIdx.x; idx < W2 * W2; idx += blockDim.x) {
-        const int c = idx / W2, k = idx - c * W2;
-        const float2 *col = (c < w ? Abuf + (size_t)c * LD : Bbuf + (size_t)(c - w) * LD) + VOFF;
-        float2 v = col[k];
-        if (k == c) v.x -= 1.f;  // exact (Sterbenz): Q_cc is within [1/2, 2]
-        Dm[k * W2 + c] = v;
-    }
-    __syncthreads();
-    // two lanes per row, 16 output columns each (32 accumulators in
-    // registers); a barrier between the reads and the write-back of a row
-    // block (uniform trip count: every thread runs every iteration)
-    constexpr int WH = W2 / 2;
-#pragma unroll 1
-    for (int base = 0; base < 2 * nc; base += blockDim.x) {
-        const int it = base + threadIdx.x;
-        const bool live = it < 2 * nc;
-        const int r = live ? it >> 1 : 0, h = it & 1;
-        float2 acc[WH];
-#pragma unroll
-        for (int c = 0; c < WH; ++c) acc[c] = make_float2(0.f, 0.f);
-        // batches of 8 input columns: the 8 L2 loads are in flight together
-#pragma unroll 1
-        for (int kb = 0; kb < W2; kb += 8) {
-            float2 v[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = kb + i;
-                const int gk = k < w ? pa * w + k : pb * w + (k - w);
-                v[i] = gk < nc ? vw[(size_t)gk * nc + r] : make_float2(0.f, 0.f);  // padding: D row is zero
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float4 *d4 = reinterpret_cast<const float4 *>(Dm + (kb + i) * W2 + h * WH);
-#pragma unroll
-                for (int c2 = 0; c2 < WH / 2; ++c2) {
-                    const float4 d = d4[c2];
-                    float2 &a0 = acc[2 * c2], &a1 = acc[2 * c2 + 1];
-                    a0.x = fmaf(v[i].x, d.x, fmaf(-v[i].y, d.y, a0.x));
-                    a0.y = fmaf(v[i].x, d.y, fmaf(v[i].y, d.x, a0.y));
-                    a1.x = fmaf(v[i].x, d.z, fmaf(-v[i].y, d.w, a1.x));
-                    a1.y = fmaf(v[i].x, d.w, fmaf(v[i].y, d.z, a1.y));
-                }
-            }
-        }
-        __syncthreads();  // the row block is read by both of its lanes
-        if (live) {
-#pragma unroll
-            for (int c = 0; c < WH; ++c) {
-                const int cc = h * WH + c;
-                const int gc = cc < w ? pa * w + cc : pb * w + (cc - w);
-                if (gc < nc) {
-                    float2 *p = vw + (size_t)gc * nc + r;
-                    float2 o = *p;
-                    o.x += acc[c].x;
-                    o.y += acc[c].y;
-                    *p = o;
-                }
-            }
-        }
-    }
-    __syncthreads();  // Dm free, V stores issued before the panels move
-}
-template <typename T>
-__device__ __forceinline__ void dv_apply_t(const cplx_t<T> *Abuf, const cplx_t<T> *Bbuf, int pa, int pb,
-                                           int w, int LD, int VOFF, cplx_t<T> *Dm, cplx_t<T> *vw, int nc) {
-    if constexpr (sizeof(T) == 4) dv_apply(Abuf, Bbuf, pa, pb, w, LD, VOFF, Dm, vw, nc);
-}
-
-
-// Warp-pair hand-off for the cross rounds when one warp is one pair slot
-// (G == 32): b_j is touched in round sr by slot j - sr only, so slot k's
-// round sr needs exactly slot k+1's round sr-1 (its b column).  A per-slot
-// round counter (release by lane 0 after __syncwarp, acquire by every lane)
-// replaces the CTA barrier: warps drift apart and one warp's shuffle /
-// parameter latency overlaps another's FMA work.  The ring k <- k+1 bounds
-// the drift; the super-round boundary is a full (cluster) barrier.
-__device__ __forceinline__ void slot_publish(int *ctr, int v) {
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(ctr)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void slot_wait(const int *ctr, int v) {
-    int x;
-    do {
-        asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(x) : "r"(smem_u32(ctr)) : "memory");
-    } while (x < v);
-}
-
 // 2C-1 super-rounds of cross pairs a x b: the a panel lives in registers, b
 // columns are read/written in shared memory; between super-rounds the panels
 // rotate across the cluster (DSMEM pulls).  The current b buffer index is
 // kept in flags[2].  Returns bit0 = rotated, bit1 = non-finite.
-template <typename T, int C, int RPLX, int RPLV, bool DV = false>
+template <typename T, int C, int RPLX, int RPLV>
 __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, int rank,
-                                        cplx_t<T> *Abuf, cplx_t<T> *Bbuf0, T tol,
-                                        cplx_t<T> *vw = nullptr) {
+                                        cplx_t<T> *Abuf, cplx_t<T> *Bbuf0, T tol) {
     using T2 = cplx_t<T>;
     constexpr bool WANTV = RPLV > 0;
     constexpr int RPLV1 = WANTV ? RPLV : 1;
@@ -334,14 +220,6 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
     const size_t panel_elems = (size_t)w * LD;
     int bcur = flags[2];
     cplx_t<T> *Bbuf = Bbuf0 + (size_t)bcur * panel_elems;
-    // warp-pair hand-off instead of CTA barriers (see slot_wait); CS_WSYNC=0 off
-    int *rctr = flags + 4 + 64;
-    const bool wsync = !DV && s.wsync && G == 32 && w * G == (int)blockDim.x;
-    if (wsync) {
-        if (g == 0) rctr[k] = 0;
-        __syncthreads();  // no slot may see a previous sweep's count
-    }
-    const int knext = (k + 1 == w) ? 0 : k + 1;
             // ---- a panel -> registers -------------------------------------
             T2 ra[RPLX], rav[RPLV1];
             if (active) {
@@ -353,16 +231,6 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
             // ---- 2C-1 super-rounds of cross pairs ---------------------------
 #pragma unroll 1
             for (int t = 0; t < 2 * C - 1; ++t) {
-                bool rot_t = false;
-                if constexpr (DV) {  // Q <- I for this super-round (a: registers, b: smem)
-#pragma unroll
-                    for (int i = 0; i < RPLV1; ++i) rav[i] = mk<T>(g + G * i == k ? (T)1 : (T)0, (T)0);
-                    for (int idx = tid; idx < w * 2 * w; idx += blockDim.x) {
-                        const int c = idx / (2 * w), r = idx - c * (2 * w);
-                        Bbuf[(size_t)c * LD + VOFF + r] = mk<T>(r == w + c ? (T)1 : (T)0, (T)0);
-                    }
-                    __syncthreads();
-                }
 #pragma unroll 1
                 for (int sr = 0; sr < w; ++sr) {
                     int j = k + sr;
@@ -370,10 +238,15 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                     T2 y[RPLX], yv[RPLV1];
                     T al = 0, be = 0, gr = 0, gi = 0;
                     const uint32_t ab = smem_u32(Bbuf) + j * colb + g * T2SZ;
-                    if (wsync && sr > 0) slot_wait(rctr + knext, t * w + sr);
                     if (active) {
                         col_load<T, RPLX>(y, ab, rstride);
-                        pair_dots<T, RPLX>(ra, y, al, be, gr, gi);
+#pragma unroll
+                        for (int i = 0; i < RPLX; ++i) {
+                            al = fma(ra[i].y, ra[i].y, fma(ra[i].x, ra[i].x, al));
+                            be = fma(y[i].y, y[i].y, fma(y[i].x, y[i].x, be));
+                            gr = fma(ra[i].y, y[i].y, fma(ra[i].x, y[i].x, gr));
+                            gi = fma(-ra[i].y, y[i].x, fma(ra[i].x, y[i].y, gi));
+                        }
                     }
 #pragma unroll
                     for (int off = 16; off >= 1; off >>= 1) {
@@ -391,7 +264,6 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                             bad = true;
                         } else if (act > 0) {
                             rot = true;
-                            if constexpr (DV) rot_t = true;
                             if constexpr (GCHECK_BUILT<T, RPLX, RPLV>) big |= act > 1;
 #pragma unroll
                             for (int i = 0; i < RPLX; ++i) rot_apply<T>(ra[i], y[i], R);
@@ -404,21 +276,7 @@ __device__ __noinline__ int panel_cross(const JacShape &s, unsigned char *smem, 
                             }
                         }
                     }
-                    if (wsync) {
-                        __syncwarp();
-                        if (g == 0) slot_publish(rctr + k, t * w + sr + 1);
-                    } else {
-                        __syncthreads();
-                    }
-                }
-                if (wsync) __syncthreads();  // all rounds of the super-round done
-                if constexpr (DV) {  // back-transform V's 2w columns by this super-round's Q
-                    if (__syncthreads_or(rot_t)) {
-                        if (active) col_store<T, RPLV1>(rav, smem_u32(Abuf) + k * colb + g * T2SZ + voff_b, rstride);
-                        __syncthreads();
-                        cplx_t<T> *Dm = Bbuf0 + (size_t)(bcur ^ 1) * panel_elems;  // spare buffer
-                        dv_apply_t<T>(Abuf, Bbuf, pos[rank], pos[2 * C - 1 - rank], w, LD, VOFF, Dm, vw, s.nc);
-                    }
+                    __syncthreads();
                 }
                 if constexpr (C > 1) {
                     if (t == 2 * C - 2) break;
@@ -1247,8 +1105,8 @@ __device__ __noinline__ int gram_check(const JacShape &s, unsigned char *smem, i
     return any;
 }
 
-template <typename T, int C, int RPLX, int RPLV, bool SPLIT, bool DV = false>
-__global__ void __launch_bounds__((DV && RPLX == 16) ? 256 : (SPLIT ? 1024 : JAC_MAX_THREADS), (DV && RPLX == 16) ? 2 : 1)
+template <typename T, int C, int RPLX, int RPLV, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 1024 : JAC_MAX_THREADS)
 jacobi_panel_kernel(const JacArgs<T> a) {
     using T2 = cplx_t<T>;
     constexpr bool WANTV = RPLV > 0;
@@ -1258,8 +1116,6 @@ jacobi_panel_kernel(const JacArgs<T> a) {
     int rank = 0;
     if constexpr (C > 1) rank = (int)cg::this_cluster().block_rank();
     const long long cid = blockIdx.x / C;
-    // DV: this cluster's V (column-major nc x nc) in the global workspace
-    cplx_t<T> *vw = DV ? a.scratch + (size_t)cid * s.nc * s.nc : nullptr;
 
     const int w = s.P;            // panel width (pairs per round)
     const int G = s.G;
@@ -1316,23 +1172,7 @@ jacobi_panel_kernel(const JacArgs<T> a) {
                     }
                     dst[(size_t)jj * LD + r] = v;
                 }
-                if constexpr (DV) {
-                    // Q rows <- identity; V columns of this panel -> workspace
-                    const int rows_v = G * RPLV;
-                    for (int idx = tid; idx < w * rows_v; idx += blockDim.x) {
-                        const int jj = idx / rows_v, r = idx - jj * rows_v;
-                        dst[(size_t)jj * LD + VOFF + r] = mk<T>(r == half * w + jj ? (T)1 : (T)0, 0);
-                    }
-                    const int nc_ = s.nc;
-                    for (int idx = tid; idx < w * nc_; idx += blockDim.x) {
-                        int jj, r;
-                        if (V0) { r = idx / w; jj = idx - r * w; }
-                        else { jj = idx / nc_; r = idx - jj * nc_; }
-                        const int j = c0 + jj;
-                        if (j >= nc_) continue;
-                        vw[(size_t)j * nc_ + r] = V0 ? V0[(size_t)r * nc_ + j] : mk<T>(r == j ? (T)1 : (T)0, 0);
-                    }
-                } else if constexpr (WANTV) {
+                if constexpr (WANTV) {
                     const int rows_v = G * RPLV;
                     for (int idx = tid; idx < w * rows_v; idx += blockDim.x) {
                         int jj, r;
@@ -1363,16 +1203,6 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             } else if (s.gram) {
                 fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
                 fl |= panel_cross_gram<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
-            } else if constexpr (DV) {
-                if (sweep > 0) {
-                    dv_reset_q<T>(Abuf, Bbuf, w, LD, VOFF);
-                    __syncthreads();
-                }
-                fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
-                if (__syncthreads_or(fl & 1))
-                    dv_apply_t<T>(Abuf, Bbuf, start_a, start_b, w, LD, VOFF,
-                                  Bbuf0 + (size_t)(flags[2] ^ 1) * panel_elems, vw, nc);
-                fl |= panel_cross<T, C, RPLX, RPLV, true>(s, smem, rank, Abuf, Bbuf0, tol, vw);
             } else {
 #ifdef CS_PHASE_CLOCKS
                 long long c0 = clock64();
@@ -1501,22 +1331,7 @@ jacobi_panel_kernel(const JacArgs<T> a) {
                         a.Uw[((size_t)mid * mr + r) * nc + ipos[j]] = mk<T>(epi_div(v.x, den), epi_div(v.y, den));
                     }
                 }
-                if (a.Vw && DV) {
-                    // stage this panel's V columns from the workspace over its X rows
-                    // (U is written), then emit them like the in-panel path
-                    __syncthreads();
-                    T2 *stg = const_cast<T2 *>(src);
-                    for (int idx = tid; idx < w * nc; idx += blockDim.x) {
-                        const int jj = idx / nc, r = idx - jj * nc, j = c0 + jj;
-                        if (j < nc) stg[(size_t)jj * LD + r] = vw[(size_t)j * nc + r];
-                    }
-                    __syncthreads();
-                    for (int idx = tid; idx < nc * w; idx += blockDim.x) {
-                        const int r = idx / w, jj = idx - r * w, j = c0 + jj;
-                        if (j >= nc) continue;
-                        a.Vw[((size_t)mid * nc + r) * nc + ipos[j]] = stg[(size_t)jj * LD + r];
-                    }
-                } else if (a.Vw) {
+                if (a.Vw) {
                     for (int idx = tid; idx < nc * w; idx += blockDim.x) {
                         const int r = idx / w, jj = idx - r * w, j = c0 + jj;
                         if (j >= nc) continue;

@@ -412,34 +412,3 @@ def test_gram_check_matches_check_sweep(cuda, orc, monkeypatch, shape, count, ve
             assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= bar * s[f][0]
             assert np.abs(U[f].conj().T @ U[f] - np.eye(r)).max() <= 10 * bar
             assert np.abs(V[f].conj().T @ V[f] - np.eye(r)).max() <= 10 * bar
-
-
-@pytest.mark.parametrize("shape,count", [((256, 256), 200), ((250, 256), 150), ((256, 240), 150),
-                                         ((160, 160), 120)])
-def test_deferred_v_matches_oracle_and_in_panel_v(cuda, orc, monkeypatch, shape, count):
-    """Deferred-V panel path (cs_panel.cuh DV: Q rows in the panels, V
-    back-transformed by batched GEMMs in a global workspace) against the
-    oracle and against the in-panel V path (CS_DV=0): sigma at the fp32 bar,
-    orthonormal factors, reconstruction.  The shapes cover padded panel
-    columns (nc < 2Cw), wide blocks and rows below 256."""
-    co, ci = shape
-    rng = np.random.default_rng(co * 3 + ci)
-    A = (rng.standard_normal((count, co, ci)) + 1j * rng.standard_normal((count, co, ci))) / np.sqrt(ci)
-    blocks = torch.from_numpy(A.astype(np.complex64)).to(cuda)
-    outs = {}
-    for mode in ("1", "0"):
-        monkeypatch.setenv("CS_DV", mode)
-        outs[mode] = engine.batched_svd(blocks, "f32", True)
-    monkeypatch.delenv("CS_DV")
-    ref, _ = orc.svd_values(A)
-    r = min(co, ci)
-    for mode, out in outs.items():
-        assert (out.info.cpu().numpy() > 0).all(), mode
-        assert per_freq_rel_err(out.sigma.cpu().numpy(), ref).max() <= TOL32, mode
-        U = out.U.cpu().numpy().astype(np.complex128)
-        V = out.V.cpu().numpy().astype(np.complex128)
-        s = out.sigma.cpu().numpy().astype(np.float64)
-        for f in range(0, count, max(1, count // 10)):
-            assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= TOL32 * s[f][0], mode
-            assert np.abs(U[f].conj().T @ U[f] - np.eye(r)).max() <= 10 * TOL32, mode
-            assert np.abs(V[f].conj().T @ V[f] - np.eye(r)).max() <= 10 * TOL32, mode
