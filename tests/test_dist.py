@@ -14,7 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2506_05617_b200 import engine
-from paper_2506_05617_b200.distributed import gather_sigma, shard_range
+from paper_2506_05617_b200.distributed import gather_factors, gather_sigma, shard_range
 
 
 @pytest.mark.parametrize("total", [1, 7, 514, 32770])
@@ -71,3 +71,40 @@ def test_gather_sigma_world2_gloo():
     rep_of, _ = engine.partner_map(n, m)
     values = np.sort(full[rep_of].ravel())[::-1]
     assert len(values) == n * m * r
+
+
+def _factor_worker(rank, world, port, total, rows, r, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    u0, cnt = shard_range(total, rank, world)
+    # shard u of the factor: entries u + 1j * (row * r + col)
+    idx = torch.arange(u0, u0 + cnt, dtype=torch.float32)[:, None, None]
+    im = torch.arange(rows * r, dtype=torch.float32).reshape(1, rows, r)
+    shard = torch.complex(idx.expand(cnt, rows, r), im.expand(cnt, rows, r)).contiguous()
+    full = gather_factors(shard, total, dst=world - 1)
+    if rank == world - 1:
+        q.put(full.numpy())
+    else:
+        assert full is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 11), (3, 10)])
+def test_gather_factors_to_one_rank_gloo(world, total):
+    """U/V shards to one rank by grouped point-to-point sends."""
+    rows, r = 4, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_factor_worker, args=(g, world, port, total, rows, r, q))
+             for g in range(world)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert full.shape == (total, rows, r)
+    assert np.array_equal(full.real, np.broadcast_to(np.arange(total)[:, None, None], (total, rows, r)))
+    assert np.array_equal(full.imag, np.broadcast_to(np.arange(rows * r).reshape(1, rows, r), (total, rows, r)))

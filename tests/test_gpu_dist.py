@@ -73,3 +73,57 @@ def test_two_ranks_match_single(cuda, cfg):
     for _, u0, cnt, vals, sig in outs:
         assert np.abs(vals - ref_vals).max() <= 2e-6 * ref_vals[0]
         assert np.abs(sig - ref_sig[u0:u0 + cnt]).max() <= 2e-6 * ref_vals[0]
+
+
+def _vec_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2506_05617_b200 import configs, engine
+    from paper_2506_05617_b200.distributed import gather_sigma, lfa_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    layer = configs.WORKLOADS[2].layers[0]
+    w = torch.from_numpy(configs.layer_weights(layer)).cuda()
+    res = lfa_sharded(w, layer.n, layer.m, "f32", True, gather_vectors_to=1)
+    full = gather_sigma(res.sigma, engine.half_grid_count(layer.n, layer.m))
+    if rank == 1:
+        blocks = engine.symbol_field(w, layer.n, layer.m, "f32", half=True)
+        F_u = blocks.shape[0]
+        worst = 0.0
+        for u in np.unique(np.linspace(0, F_u - 1, 16).astype(int)):
+            A = blocks[u].cpu().numpy().astype(np.complex128)
+            U = res.U[u].cpu().numpy().astype(np.complex128)
+            V = res.V[u].cpu().numpy().astype(np.complex128)
+            s = full[u].cpu().numpy().astype(np.float64)
+            worst = max(worst, np.abs((U * s) @ V.conj().T - A).max() / s[0])
+        q.put((res.U.shape[0], F_u, worst))
+    else:
+        q.put((res.U is None, res.V is None, 0.0))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gather_vectors_to_one_rank(cuda):
+    """U/V shards moved to one rank (distributed.gather_factors) reconstruct
+    every sampled block with the all-gathered sigma."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vec_worker, args=(g, 2, port, q)) for g in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for a, b, worst in outs:
+        if a is True:
+            assert b is True  # rank 0 keeps nothing
+        else:
+            assert a == b and worst <= 1e-5
