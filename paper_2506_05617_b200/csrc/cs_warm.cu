@@ -7,9 +7,13 @@
 // exact fp32 arithmetic), and V accumulates from V_{f'}
 // so U/V come out directly.  This file forms X' for a batch with one tiled
 // complex GEMM: out[i] = X_{wid[i]} . Vw[sid[i]].
+#include <cstdlib>
+
 #include "cs_common.cuh"
 
 namespace cs {
+
+__device__ __forceinline__ uint32_t smem_u32c(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 constexpr int WG_TILE = 64, WG_K = 8, WG_THREADS = 256;
 
@@ -79,6 +83,172 @@ warm_gemm_kernel(const cplx_t<T> *__restrict__ blocks, int co, int ci, int wide,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core path (fp32, tall blocks, mr % 128 == 0, nc % 64 == 0): the same
+// out = X . V on the 5th-gen tensor cores.  A CTA owns a 128 x 64 complex
+// output tile = a 128 x 128 real TMEM accumulator [X_r | X_i]:
+//   A_op (128 x 2K real, K-major)  = [A_r | A_i]
+//   B_op (128 x 2K real, K-major)  rows n < 64: [V_r(:,n) | -V_i(:,n)],
+//                                  rows 64+n:   [V_i(:,n) |  V_r(:,n)]
+// K is staged 32 complex (64 real) at a time into the canonical no-swizzle
+// K-major layout (8-row x 16-byte core matrices, LBO 128 B, SBO 2 KB), split
+// into hi = tf32(x) and lo = x - hi on the fly; each K step of 8 issues
+// hi*hi + hi*lo + lo*hi (3xTF32: fp32-level products, tools/tc_probe.cu:
+// 9.5e-7 relative) from one elected thread; tcgen05.commit -> mbarrier
+// orders the restaging.  The epilogue reads TMEM with tcgen05.ld.
+// ---------------------------------------------------------------------------
+constexpr int TC_M = 128, TC_NC = 64, TC_KC = 16;   // rows, complex cols, complex K per stage
+constexpr int TC_KR = 2 * TC_KC;                     // real K per stage
+constexpr int TC_LBO = 128, TC_SBO = (TC_KR / 4) * 128;
+constexpr int TC_THREADS = 256;
+constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                              ((uint32_t)(TC_M >> 4) << 24);  // kind::tf32, f32 acc, K-major, 128x128
+
+__device__ __forceinline__ int tc_canon(int r, int k) {
+    return (r & 7) * 4 + (r >> 3) * (TC_SBO / 4) + (k & 3) + (k >> 2) * (TC_LBO / 4);
+}
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(TC_LBO >> 4) << 16) |
+           ((uint64_t)(TC_SBO >> 4) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
+}
+__device__ __forceinline__ void tc_split(float x, float &hi, float &lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    lo = x - hi;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 2)
+warm_gemm_tc_kernel(const float2 *__restrict__ blocks, int co, int ci, const long long *__restrict__ wid,
+                    const long long *__restrict__ sid, const float2 *__restrict__ Vw,
+                    float2 *__restrict__ out) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    float *Ah = reinterpret_cast<float *>(tsm), *Al = Ah + TC_M * TC_KR;
+    float *Bh = Al + TC_M * TC_KR, *Bl = Bh + 128 * TC_KR;
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t mbar;
+    const int mr = co, nc = ci;
+    const long long item = blockIdx.z;
+    const float2 *A = blocks + (size_t)wid[item] * co * ci;
+    const float2 *V = Vw + (size_t)sid[item] * nc * nc;
+    float2 *O = out + (size_t)item * mr * nc;
+    const int row0 = blockIdx.y * TC_M, col0 = blockIdx.x * TC_NC;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32c(&tmem_base)),
+                     "r"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32c(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const int nstage = nc / TC_KC;
+    // warp w owns TMEM lanes 32*(w%4).. (rows) and complex columns [nb, nb+32):
+    // X_r at TMEM column n, X_i at 64 + n.  Each stage's 64 real K terms are
+    // summed by the tensor cores into a fresh accumulator and the stages are
+    // added here in fp32 (accumulating all 2*nc terms in TMEM measured 5.5e-6
+    // relative error at nc = 256; per stage it stays at the 3xTF32 product level)
+    const int rr = 32 * (warp & 3) + lane, nb = 32 * (warp >> 2);
+    const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    float accr[32], acci[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) accr[i] = acci[i] = 0.f;
+    for (int kc = 0; kc < nstage; ++kc) {
+        const int k0 = kc * TC_KC;
+        // A_op: 128 rows x 32 complex k -> reals (k | 32 + k)
+        for (int x = tid; x < TC_M * TC_KC; x += TC_THREADS) {
+            const int r = x / TC_KC, k = x % TC_KC;
+            const float2 a = A[(size_t)(row0 + r) * ci + k0 + k];
+            float h, l;
+            tc_split(a.x, h, l);
+            Ah[tc_canon(r, k)] = h;
+            Al[tc_canon(r, k)] = l;
+            tc_split(a.y, h, l);
+            Ah[tc_canon(r, TC_KC + k)] = h;
+            Al[tc_canon(r, TC_KC + k)] = l;
+        }
+        // B_op: V rows k0..k0+31, complex cols col0..col0+63
+        for (int x = tid; x < TC_KC * TC_NC; x += TC_THREADS) {
+            const int k = x / TC_NC, n = x % TC_NC;
+            const float2 v = V[(size_t)(k0 + k) * nc + col0 + n];
+            float h, l;
+            tc_split(v.x, h, l);  // V_r
+            Bh[tc_canon(n, k)] = h;
+            Bl[tc_canon(n, k)] = l;
+            Bh[tc_canon(64 + n, TC_KC + k)] = h;
+            Bl[tc_canon(64 + n, TC_KC + k)] = l;
+            tc_split(v.y, h, l);  // V_i
+            Bh[tc_canon(64 + n, k)] = h;
+            Bl[tc_canon(64 + n, k)] = l;
+            Bh[tc_canon(n, TC_KC + k)] = -h;
+            Bl[tc_canon(n, TC_KC + k)] = -l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a[2] = {smem_u32c(Ah), smem_u32c(Al)}, b[2] = {smem_u32c(Bh), smem_u32c(Bl)};
+#pragma unroll
+            for (int ks = 0; ks < TC_KR / 8; ++ks)
+#pragma unroll
+                for (int p = 0; p < 3; ++p) {
+                    const uint64_t da = tc_desc(a[p == 2 ? 1 : 0] + ks * 2 * TC_LBO);
+                    const uint64_t db = tc_desc(b[p == 1 ? 1 : 0] + ks * 2 * TC_LBO);
+                    const uint32_t acc = (ks | p) ? 1u : 0u;
+                    asm volatile(
+                        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n\t}" ::"r"(tmem),
+                        "l"(da), "l"(db), "r"(TC_IDESC), "r"(acc));
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32c(&mbar))
+                         : "memory");
+        }
+        // this stage's MMAs done: shared memory free, accumulator readable
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tTCW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra TCW_%=;\n\t}" ::"r"(smem_u32c(&mbar)), "r"(kc & 1)
+            : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t re[16], im[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(re[0]), "=r"(re[1]), "=r"(re[2]), "=r"(re[3]), "=r"(re[4]), "=r"(re[5]), "=r"(re[6]),
+                  "=r"(re[7]), "=r"(re[8]), "=r"(re[9]), "=r"(re[10]), "=r"(re[11]), "=r"(re[12]), "=r"(re[13]),
+                  "=r"(re[14]), "=r"(re[15])
+                : "r"(tl + nb + 16 * h));
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(im[0]), "=r"(im[1]), "=r"(im[2]), "=r"(im[3]), "=r"(im[4]), "=r"(im[5]), "=r"(im[6]),
+                  "=r"(im[7]), "=r"(im[8]), "=r"(im[9]), "=r"(im[10]), "=r"(im[11]), "=r"(im[12]), "=r"(im[13]),
+                  "=r"(im[14]), "=r"(im[15])
+                : "r"(tl + 64 + nb + 16 * h));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                accr[16 * h + i] += __uint_as_float(re[i]);
+                acci[16 * h + i] += __uint_as_float(im[i]);
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();  // accumulator read by all warps before the next stage's MMAs
+    }
+    float2 *orow = O + (size_t)(row0 + rr) * nc + col0 + nb;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2)
+        *reinterpret_cast<float4 *>(orow + i) = make_float4(accr[i], acci[i], accr[i + 1], acci[i + 1]);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+}
+
+constexpr size_t TC_SMEM = (size_t)(2 * TC_M * TC_KR + 2 * 128 * TC_KR) * sizeof(float);
+
 }  // namespace cs
 
 using namespace cs;
@@ -95,6 +265,21 @@ extern "C" int cs_warm_start_gemm(const void *blocks, int dtype, int c_out, int 
     const int wide = c_out < c_in;
     const int mr = wide ? c_in : c_out, nc = wide ? c_out : c_in;
     cudaStream_t st = (cudaStream_t)stream;
+    const char *tcenv = std::getenv("CS_WARM_TC");  // "0": CUDA-core kernel
+    if (dtype == CS_F32 && !wide && mr % TC_M == 0 && nc % TC_NC == 0 && !(tcenv && tcenv[0] == '0')) {
+        CS_CUDA_TRY(cudaFuncSetAttribute(warm_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TC_SMEM));
+        for (long long off = 0; off < count; off += 65535) {
+            const long long cnt = lmin(65535, count - off);
+            dim3 grid(nc / TC_NC, mr / TC_M, (unsigned)cnt);
+            warm_gemm_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(
+                (const float2 *)blocks, c_out, c_in, warm_ids + off, seed_ids + off, (const float2 *)Vw,
+                (float2 *)out_X + (size_t)off * mr * nc);
+            int s = check_launch("warm_gemm_tc_kernel");
+            if (s) return s;
+        }
+        return CS_OK;
+    }
     for (long long off = 0; off < count; off += 65535) {
         const long long cnt = lmin(65535, count - off);
         dim3 grid((nc + WG_TILE - 1) / WG_TILE, (mr + WG_TILE - 1) / WG_TILE, (unsigned)cnt);

@@ -412,3 +412,28 @@ def test_gram_check_matches_check_sweep(cuda, orc, monkeypatch, shape, count, ve
             assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= bar * s[f][0]
             assert np.abs(U[f].conj().T @ U[f] - np.eye(r)).max() <= 10 * bar
             assert np.abs(V[f].conj().T @ V[f] - np.eye(r)).max() <= 10 * bar
+
+
+@pytest.mark.parametrize("shape,count", [((256, 256), 7), ((384, 256), 3), ((128, 64), 5)])
+def test_warm_start_gemm_tensor_cores(cuda, monkeypatch, shape, count):
+    """cs_warm_start_gemm X_i = A_{wid[i]} V_{sid[i]}: the tcgen05 3xTF32 path
+    (fp32, tall, mr % 128 == 0, nc % 64 == 0) and the CUDA-core path both at
+    fp32 level against an fp64 product."""
+    co, ci = shape
+    rng = np.random.default_rng(co + 3 * ci)
+    A = (rng.standard_normal((count + 2, co, ci)) + 1j * rng.standard_normal((count + 2, co, ci))) / np.sqrt(ci)
+    V = (rng.standard_normal((count + 1, ci, ci)) + 1j * rng.standard_normal((count + 1, ci, ci))) / np.sqrt(ci)
+    wid = np.array([(3 * i + 1) % (count + 2) for i in range(count)], dtype=np.int64)
+    sid = np.array([(5 * i + 2) % (count + 1) for i in range(count)], dtype=np.int64)
+    ref = np.einsum("irk,ikc->irc", A[wid], V[sid])
+    blocks = torch.from_numpy(A.astype(np.complex64)).to(cuda)
+    Vt = torch.from_numpy(V.astype(np.complex64)).to(cuda)
+    w_t, s_t = torch.from_numpy(wid).to(cuda), torch.from_numpy(sid).to(cuda)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("CS_WARM_TC", mode)
+        out = torch.empty((count, co, ci), dtype=torch.complex64, device=cuda)
+        engine.warm_start_gemm(blocks, "f32", w_t, s_t, Vt, out)
+        got = out.cpu().numpy().astype(np.complex128)
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err <= 3e-6, (mode, err)
+    monkeypatch.delenv("CS_WARM_TC")
