@@ -187,3 +187,29 @@ def test_materialize_on_host_triplet():
         cs.materialize_singular_vector(t, 2, "left", cs.SpatialDims(4, 4))
     with pytest.raises(ValueError):
         cs.materialize_singular_vector(t, 0, "up", cs.SpatialDims(4, 4))
+
+
+@pytest.mark.parametrize("depth", [3, 8])
+@pytest.mark.parametrize("n,m,u0,count", [(256, 256, 0, None), (64, 64, 100, 900), (7, 6, 0, None)])
+def test_warm_plan_is_a_bfs_forest(depth, n, m, u0, count):
+    """engine.warm_plan: every representative of the range solved exactly
+    once; stage 0 cold seeds, every later block warm-started from a lattice
+    neighbour (|di| + |dj| == 1) solved in the previous stage."""
+    total = engine.half_grid_count(n, m)
+    count = total - u0 if count is None else count
+    plan = engine.warm_plan(n, m, u0, count, "cpu", depth)
+    reps = engine.half_grid_indices(n, m)[u0:u0 + count]
+    stage_of = np.full(count, -1)
+    for d, (ids, pred) in enumerate(plan):
+        ids = ids.numpy()
+        assert (stage_of[ids] == -1).all()
+        stage_of[ids] = d
+        if d == 0:
+            assert pred is None
+            continue
+        pred = pred.numpy()
+        assert (stage_of[pred] >= 0).all() and (stage_of[pred] < d).all()
+        di = np.abs(reps[ids] // m - reps[pred] // m)
+        dj = np.abs(reps[ids] % m - reps[pred] % m)
+        assert ((di + dj) == 1).all()
+    assert (stage_of >= 0).all()
