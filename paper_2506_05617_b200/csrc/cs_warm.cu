@@ -115,6 +115,12 @@ __device__ __forceinline__ void tc_split(float x, float &hi, float &lo) {
     hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     lo = x - hi;
 }
+__device__ __forceinline__ void tc_split4(float4 x, float4 &hi, float4 &lo) {
+    tc_split(x.x, hi.x, lo.x);
+    tc_split(x.y, hi.y, lo.y);
+    tc_split(x.z, hi.z, lo.z);
+    tc_split(x.w, hi.w, lo.w);
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 2)
 warm_gemm_tc_kernel(const float2 *__restrict__ blocks, int co, int ci, const long long *__restrict__ wid,
@@ -157,33 +163,38 @@ warm_gemm_tc_kernel(const float2 *__restrict__ blocks, int co, int ci, const lon
     for (int i = 0; i < 32; ++i) accr[i] = acci[i] = 0.f;
     for (int kc = 0; kc < nstage; ++kc) {
         const int k0 = kc * TC_KC;
-        // A_op: 128 rows x 32 complex k -> reals (k | 32 + k)
-        for (int x = tid; x < TC_M * TC_KC; x += TC_THREADS) {
-            const int r = x / TC_KC, k = x % TC_KC;
-            const float2 a = A[(size_t)(row0 + r) * ci + k0 + k];
-            float h, l;
-            tc_split(a.x, h, l);
-            Ah[tc_canon(r, k)] = h;
-            Al[tc_canon(r, k)] = l;
-            tc_split(a.y, h, l);
-            Ah[tc_canon(r, TC_KC + k)] = h;
-            Al[tc_canon(r, TC_KC + k)] = l;
+        // staging in 16-byte chunks: a chunk of the canonical layout holds 4
+        // consecutive K of one row, so each thread converts 4 complex values
+        // into four float4 stores (hi/lo of the real and imaginary parts).
+        // A_op row r: [A_r(k0..k0+KC) | A_i(k0..k0+KC)]
+        for (int it = tid; it < TC_M * (TC_KC / 4); it += TC_THREADS) {
+            const int r = it % TC_M, c4 = it / TC_M;
+            const float4 *src = reinterpret_cast<const float4 *>(A + (size_t)(row0 + r) * ci + k0 + 4 * c4);
+            const float4 p0 = src[0], p1 = src[1];  // (re0, im0, re1, im1), (re2, im2, re3, im3)
+            float4 h, l;
+            tc_split4(make_float4(p0.x, p0.z, p1.x, p1.z), h, l);
+            *reinterpret_cast<float4 *>(Ah + tc_canon(r, 4 * c4)) = h;
+            *reinterpret_cast<float4 *>(Al + tc_canon(r, 4 * c4)) = l;
+            tc_split4(make_float4(p0.y, p0.w, p1.y, p1.w), h, l);
+            *reinterpret_cast<float4 *>(Ah + tc_canon(r, TC_KC + 4 * c4)) = h;
+            *reinterpret_cast<float4 *>(Al + tc_canon(r, TC_KC + 4 * c4)) = l;
         }
-        // B_op: V rows k0..k0+31, complex cols col0..col0+63
-        for (int x = tid; x < TC_KC * TC_NC; x += TC_THREADS) {
-            const int k = x / TC_NC, n = x % TC_NC;
-            const float2 v = V[(size_t)(k0 + k) * nc + col0 + n];
-            float h, l;
-            tc_split(v.x, h, l);  // V_r
-            Bh[tc_canon(n, k)] = h;
-            Bl[tc_canon(n, k)] = l;
-            Bh[tc_canon(64 + n, TC_KC + k)] = h;
-            Bl[tc_canon(64 + n, TC_KC + k)] = l;
-            tc_split(v.y, h, l);  // V_i
-            Bh[tc_canon(64 + n, k)] = h;
-            Bl[tc_canon(64 + n, k)] = l;
-            Bh[tc_canon(n, TC_KC + k)] = -h;
-            Bl[tc_canon(n, TC_KC + k)] = -l;
+        // B_op row n < 64: [V_r(:,n) | -V_i(:,n)], row 64 + n: [V_i(:,n) | V_r(:,n)]
+        for (int it = tid; it < TC_NC * (TC_KC / 4); it += TC_THREADS) {
+            const int n = it % TC_NC, c4 = it / TC_NC;
+            const float2 *vc = V + (size_t)(k0 + 4 * c4) * nc + col0 + n;
+            const float2 v0 = vc[0], v1 = vc[nc], v2 = vc[2 * (size_t)nc], v3 = vc[3 * (size_t)nc];
+            float4 h, l;
+            tc_split4(make_float4(v0.x, v1.x, v2.x, v3.x), h, l);  // V_r
+            *reinterpret_cast<float4 *>(Bh + tc_canon(n, 4 * c4)) = h;
+            *reinterpret_cast<float4 *>(Bl + tc_canon(n, 4 * c4)) = l;
+            *reinterpret_cast<float4 *>(Bh + tc_canon(64 + n, TC_KC + 4 * c4)) = h;
+            *reinterpret_cast<float4 *>(Bl + tc_canon(64 + n, TC_KC + 4 * c4)) = l;
+            tc_split4(make_float4(v0.y, v1.y, v2.y, v3.y), h, l);  // V_i
+            *reinterpret_cast<float4 *>(Bh + tc_canon(64 + n, 4 * c4)) = h;
+            *reinterpret_cast<float4 *>(Bl + tc_canon(64 + n, 4 * c4)) = l;
+            *reinterpret_cast<float4 *>(Bh + tc_canon(n, TC_KC + 4 * c4)) = make_float4(-h.x, -h.y, -h.z, -h.w);
+            *reinterpret_cast<float4 *>(Bl + tc_canon(n, TC_KC + 4 * c4)) = make_float4(-l.x, -l.y, -l.z, -l.w);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
