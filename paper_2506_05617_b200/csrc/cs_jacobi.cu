@@ -214,6 +214,11 @@ static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     if (const char *fc = std::getenv("CS_PANEL_C")) {  // experiment hook: force the cluster size
         if (plan_panel<T>(co, ci, wantv, std::atoi(fc), s)) return true;
     }
+    if (const char *fg = std::getenv("CS_GENERIC_C")) {  // experiment hook: generic kernel, cluster C
+        const int c = std::atoi(fg);
+        if (plan_generic<T>(co, ci, wantv, c, true, s)) return true;
+        if (plan_generic<T>(co, ci, wantv, c, false, s)) return true;
+    }
     for (int i = 0; i < 5; ++i) {
         if (!plan_panel<T>(co, ci, wantv, Cs[i], s)) continue;
         int j = i;
