@@ -153,7 +153,10 @@ template <typename T> struct Rot { T cm1, wr, wi; };
 // |gamma|/sqrt(alpha beta) > GCHECK_TAU: the panel kernel runs its Gram
 // convergence check only after sweeps without such a pair (quadratic
 // convergence makes the next sweep likely rotation-free, tools/stopstudy.py).
-constexpr double GCHECK_TAU2 = 0.05 * 0.05;
+#ifndef CS_GCHECK_TAU
+#define CS_GCHECK_TAU 0.05
+#endif
+constexpr double GCHECK_TAU2 = CS_GCHECK_TAU * CS_GCHECK_TAU;
 
 template <typename T>
 __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> &R) {
