@@ -340,7 +340,20 @@ def warm_start_gemm(blocks, dtype: str, warm_ids, seed_ids, Vw, out_X):
 
 
 _WARM_PLANS = {}
-WARM_DEPTH = int(os.environ.get("CS_WARM_DEPTH", "8"))  # cfg5 warm SVD: 3 -> 4.83 s, 5 -> 4.74, 8 -> 4.72, 12 -> 4.74, 24 -> 4.77
+_WARM_DEPTH_ENV = os.environ.get("CS_WARM_DEPTH")
+
+
+def warm_depth(co: int, ci: int) -> int:
+    """Seed lattice half-period: deep chains (few cold seeds) pay for large
+    blocks, short ones (few staged launches) for small blocks.  Measured:
+    cfg5 256^2 warm SVD depth 3 -> 4.83 s, 5 -> 4.74, 8 -> 4.72, 12 -> 4.74,
+    24 -> 4.77; cfg2 64^2 step depth 3 -> 6.94 ms, 8 -> 9.05 ms (cold 7.83)."""
+    if _WARM_DEPTH_ENV is not None:
+        return int(_WARM_DEPTH_ENV)
+    return 8 if min(co, ci) >= 128 else 3
+
+
+WARM_DEPTH = int(_WARM_DEPTH_ENV) if _WARM_DEPTH_ENV is not None else 3  # warm_plan() default (no block shape)
 
 
 def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = None):
@@ -403,6 +416,8 @@ def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SV
     (cs_warm_start_gemm + cs_batched_svd_indexed), stage by stage."""
     count, co, ci = blocks.shape
     dev = blocks.device
+    if depth is None:
+        depth = warm_depth(co, ci)
     out = alloc_svd_outputs(count, co, ci, dtype, True, dev)
     wide = co < ci
     mr, nc = (ci, co) if wide else (co, ci)
