@@ -124,7 +124,9 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     while (G * 2 <= 32 && w * G * 2 <= JAC_MAX_THREADS && G * 2 * 4 <= pow2ceil(s.mr)) G *= 2;
     const int rplx = std::max(2, pow2ceil((s.mr + G - 1) / G));
     const int rplv = wantv ? rplx : 0;
-    const int budget = sizeof(T) == 4 ? 16 : 8;  // complex rows per column held in registers
+    // complex rows per column held in registers; fp64 C = 16 panels run 256
+    // threads (255 registers each) and take 16 (cfg5 in fp64, cs_jacobi_f64.cu)
+    const int budget = sizeof(T) == 4 ? 16 : ((C == 16 && w * G <= 256 && wantv) ? 16 : 8);
     // with vectors, X and V rows go to separate warps when 2x the threads fit
     // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
     s.split = (wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&

@@ -28,6 +28,10 @@ static int fast_c(const JacArgs<double> &a, bool wantv, cudaStream_t st, bool dr
 
 template <int C_, int RPL_>
 static int panel_rpl(const JacArgs<double> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
+    // 256-thread fp64 panels with 8 X + 8 V rows per lane (cfg5 in fp64: C = 16)
+    if constexpr (C_ == 16 && RPL_ == 8)
+        if (wantv && !a.s.split)
+            return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, 8, 8, false>, a, st, dry, ncl);
     if constexpr (2 * RPL_ <= 8 && false)
         if (wantv && a.s.split)
             return launch_cluster_kernel<double, C_>(jacobi_panel_kernel<double, C_, RPL_, RPL_, true>, a, st, dry, ncl);

@@ -1106,7 +1106,7 @@ __device__ __noinline__ int gram_check(const JacShape &s, unsigned char *smem, i
 }
 
 template <typename T, int C, int RPLX, int RPLV, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? 1024 : JAC_MAX_THREADS)
+__global__ void __launch_bounds__(SPLIT ? 1024 : ((sizeof(T) == 8 && RPLX + RPLV > 8) ? 256 : JAC_MAX_THREADS))
 jacobi_panel_kernel(const JacArgs<T> a) {
     using T2 = cplx_t<T>;
     constexpr bool WANTV = RPLV > 0;

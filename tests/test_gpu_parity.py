@@ -437,3 +437,26 @@ def test_warm_start_gemm_tensor_cores(cuda, monkeypatch, shape, count):
         err = np.abs(got - ref).max() / np.abs(ref).max()
         assert err <= 3e-6, (mode, err)
     monkeypatch.delenv("CS_WARM_TC")
+
+
+def test_fp64_cfg5_shape_panel_path(cuda, orc):
+    """fp64 256x256 blocks with vectors (cfg5 in the parity precision) run the
+    256-thread C = 16 panel kernel: sigma at the 1e-10 bar against the oracle,
+    orthonormal factors and reconstruction at fp64 level."""
+    co = ci = 256
+    count = 24
+    rng = np.random.default_rng(2560)
+    A = (rng.standard_normal((count, co, ci)) + 1j * rng.standard_normal((count, co, ci))) / np.sqrt(ci)
+    assert engine.plan_kind(32770, co, ci, "f64", True) == 2  # the panel kernel
+    blocks = torch.from_numpy(A).to(cuda)
+    out = engine.batched_svd(blocks, "f64", True)
+    ref, _ = orc.svd_values(A)
+    assert (out.info.cpu().numpy() > 0).all()
+    assert per_freq_rel_err(out.sigma.cpu().numpy(), ref).max() <= 1e-10
+    U = out.U.cpu().numpy()
+    V = out.V.cpu().numpy()
+    s = out.sigma.cpu().numpy()
+    for f in range(0, count, 5):
+        assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= 1e-10 * s[f][0]
+        assert np.abs(U[f].conj().T @ U[f] - np.eye(ci)).max() <= 1e-9
+        assert np.abs(V[f].conj().T @ V[f] - np.eye(ci)).max() <= 1e-9
