@@ -223,10 +223,13 @@ static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     }
     for (int i = 0; i < 5; ++i) {
         if (!plan_panel<T>(co, ci, wantv, Cs[i], s)) continue;
+        // small batches: spread each matrix over more CTAs while fewer than
+        // 4 CTAs per SM would be queued (cfg4's 394 128^2 blocks: C = 1 19.0 ms,
+        // C = 2 12.0 ms, C = 4 13.4 ms; with a 2-per-SM cut they stayed at C = 1)
         int j = i;
-        while (j < 4 && count * Cs[j] < 2LL * num_sms()) {
-            JacShape t;
-            if (!plan_panel<T>(co, ci, wantv, Cs[j + 1], t) || t.P < 4) break;
+        while (j < 4 && count * Cs[j] < 4LL * num_sms()) {
+            JacShape t;  // panels narrower than 8 columns only add exchanges (cfg1 16^2)
+            if (!plan_panel<T>(co, ci, wantv, Cs[j + 1], t) || t.P < 8) break;
             ++j;
         }
         return plan_panel<T>(co, ci, wantv, Cs[j], s);
