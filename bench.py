@@ -449,8 +449,9 @@ def run_ours(args, wl, rank, world, local_rank):
     for l in (layers if not (len(layers) > 1 and world == 1) else []):
         total = half_count(l.n, l.m)
         u0, cnt = (0, total) if world == 1 else shard_range(total, rank, world)
-        if engine.use_warm_start(cnt, l.c_out, l.c_in, dt, wl.vectors):
-            stages = len(engine.warm_plan(l.n, l.m, u0, cnt, dev, engine.warm_depth(l.c_out, l.c_in)))
+        if (engine.use_warm_start(cnt, l.c_out, l.c_in, dt, wl.vectors) or
+                (not wl.vectors and engine.use_warm_values(cnt, l.c_out, l.c_in, dt))):
+            stages = len(engine.warm_plan(l.n, l.m, u0, cnt, dev, engine.warm_depth(cnt)))
             per_step += 1 + stages + (stages - 1) + 1
         else:
             per_step += 1 + 1 + (1 if wl.vectors else 0)

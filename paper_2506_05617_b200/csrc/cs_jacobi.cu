@@ -123,13 +123,16 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     int G = 1;
     while (G * 2 <= 32 && w * G * 2 <= JAC_MAX_THREADS && G * 2 * 4 <= pow2ceil(s.mr)) G *= 2;
     const int rplx = std::max(2, pow2ceil((s.mr + G - 1) / G));
-    const int rplv = wantv ? rplx : 0;
+    // V rows per lane: nc rows (tall blocks: fewer than the mr X rows); fp32
+    // panels carry rplx or rplx/2 (cs_jacobi_f32.cu instantiates both)
+    const int rplv = !wantv ? 0
+                     : (sizeof(T) == 4 ? std::max(rplx / 2, std::max(2, pow2ceil((s.nc + G - 1) / G))) : rplx);
     // complex rows per column held in registers; fp64 C = 16 panels run 256
     // threads (255 registers each) and take 16 (cfg5 in fp64, cs_jacobi_f64.cu)
     const int budget = sizeof(T) == 4 ? 16 : ((C == 16 && w * G <= 256 && wantv) ? 16 : 8);
     // with vectors, X and V rows go to separate warps when 2x the threads fit
     // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
-    s.split = (wantv && sizeof(T) == 4 && 2 * w * G <= 1024 && w * G % 32 == 0 &&
+    s.split = (wantv && sizeof(T) == 4 && rplv == rplx && 2 * w * G <= 1024 && w * G % 32 == 0 &&
                rplx <= budget / 2 && std::getenv("CS_SPLIT") != nullptr) ? 1 : 0;  // opt-in: spills at 64 regs
     if (!s.split && rplx + rplv > budget) return false;
     s.G = G;

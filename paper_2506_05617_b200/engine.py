@@ -343,14 +343,16 @@ _WARM_PLANS = {}
 _WARM_DEPTH_ENV = os.environ.get("CS_WARM_DEPTH")
 
 
-def warm_depth(co: int, ci: int) -> int:
-    """Seed lattice half-period: deep chains (few cold seeds) pay for large
-    blocks, short ones (few staged launches) for small blocks.  Measured:
-    cfg5 256^2 warm SVD depth 3 -> 4.83 s, 5 -> 4.74, 8 -> 4.72, 12 -> 4.74,
-    24 -> 4.77; cfg2 64^2 step depth 3 -> 6.94 ms, 8 -> 9.05 ms (cold 7.83)."""
+def warm_depth(count: int) -> int:
+    """Seed lattice half-period: deep chains (few cold seeds) pay when there
+    are many blocks per stage, short ones (few staged launches) otherwise.
+    Measured: cfg5 (32770 blocks) warm SVD depth 3 -> 4.83 s, 5 -> 4.74,
+    8 -> 4.72, 12 -> 4.74, 24 -> 4.77; cfg2 (2050) step depth 3 -> 6.94 ms,
+    8 -> 9.05 ms (cold 7.83); cfg3 (1570) depth 2/3 -> 59.1 ms, 5 -> 62.6,
+    8 -> 68.8 (cold 78.0)."""
     if _WARM_DEPTH_ENV is not None:
         return int(_WARM_DEPTH_ENV)
-    return 8 if min(co, ci) >= 128 else 3
+    return 8 if count >= 16384 else 3
 
 
 WARM_DEPTH = int(_WARM_DEPTH_ENV) if _WARM_DEPTH_ENV is not None else 3  # warm_plan() default (no block shape)
@@ -417,7 +419,7 @@ def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SV
     count, co, ci = blocks.shape
     dev = blocks.device
     if depth is None:
-        depth = warm_depth(co, ci)
+        depth = warm_depth(count)
     out = alloc_svd_outputs(count, co, ci, dtype, True, dev)
     wide = co < ci
     mr, nc = (ci, co) if wide else (co, ci)
@@ -444,6 +446,17 @@ def use_warm_start(count: int, co: int, ci: int, dtype: str, want_vectors: bool,
     if not requested or count < 3:
         return False
     return plan_kind(count, co, ci, dtype, True) == 2
+
+
+def use_warm_values(count: int, co: int, ci: int, dtype: str) -> bool:
+    """Values-only solve of tall blocks through the warm-started vectors path
+    (U/V computed and dropped): with nc <= mr/2 the V rows cost at most half
+    the X rows, and the warm start halves the sweeps (cfg3 256x128).
+    CS_WARM_VALUES=0 disables."""
+    if os.environ.get("CS_WARM_VALUES") == "0" or dtype != "f32" or count < 3:
+        return False
+    mr, nc = max(co, ci), min(co, ci)
+    return nc >= 64 and mr >= 2 * nc and plan_kind(count, co, ci, dtype, True) == 2
 
 
 def complete_zero_columns(out: SvdBatch, co: int, ci: int, dtype: str):

@@ -66,7 +66,8 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
     if timer:
         timer.mark("t1")
     co, ci = w_dev.shape[0], w_dev.shape[1]
-    if engine.use_warm_start(count, co, ci, dtype, want_vectors, warm_start):
+    if (engine.use_warm_start(count, co, ci, dtype, want_vectors, warm_start) or
+            (not want_vectors and warm_start is None and engine.use_warm_values(count, co, ci, dtype))):
         out = engine.batched_svd_warm(fld, dtype, n, m, u0, tol, max_sweeps)
         if not want_vectors:
             out.U = out.V = None

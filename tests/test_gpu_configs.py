@@ -196,3 +196,19 @@ def test_fp64_sampled_frequencies(cuda, golden, key):
     out = engine.batched_svd(blocks, "f64", False)
     assert (out.info.cpu().numpy() > 0).all()
     assert per_freq_rel_err(out.sigma.cpu().numpy(), golden[key + "_sigma"]).max() <= 1e-10
+
+
+def test_tall_values_via_warm_vectors_matches_cold(cuda, monkeypatch):
+    """cfg3 (256x128, values only) solved through the warm-started vectors
+    path (engine.use_warm_values; V rows at half the X rows per lane) agrees
+    with the cold values-only solve."""
+    layer = configs.WORKLOADS[3].layers[0]
+    w = torch.from_numpy(configs.layer_weights(layer)).to(cuda)
+    assert engine.use_warm_values(engine.half_grid_count(layer.n, layer.m), layer.c_out, layer.c_in, "f32")
+    warm = lfa_device(w, layer.n, layer.m, "f32", False)
+    monkeypatch.setenv("CS_WARM_VALUES", "0")
+    cold = lfa_device(w, layer.n, layer.m, "f32", False)
+    monkeypatch.delenv("CS_WARM_VALUES")
+    assert warm.U is None and warm.V is None
+    assert per_freq_rel_err(warm.sigma.cpu().numpy(), cold.sigma.cpu().numpy()).max() <= 2e-6
+    assert warm.info.float().mean() < cold.info.float().mean()
