@@ -341,9 +341,9 @@ def run_ours(args, wl, rank, world, local_rank):
                     "algorithmic": "Golub-Reinsch sigma+U+V count x4 complex per unique block "
                                    "(SURVEY 8(d)); Jacobi executes ~3.5x more"}
         # DRAM traffic per step from the committed ncu capture of this workload
-        # (profiles/r01d_traffic_cfg5.json; null for other workloads / N > 1)
+        # (profiles/r01k_traffic_cfg5.json; null for other workloads / N > 1)
         trf = {}
-        tpath = os.path.join(ROOT, "profiles", "r01d_traffic_cfg5.json")
+        tpath = os.path.join(ROOT, "profiles", "r01k_traffic_cfg5.json")
         if world == 1 and os.path.exists(tpath):
             tj = json.load(open(tpath))
             if tj.get("workload") == workload_config(wl, world).get("workload"):
@@ -351,7 +351,7 @@ def run_ours(args, wl, rank, world, local_rank):
         if "jacobi_panel_kernel" in trf:
             j = trf["jacobi_panel_kernel"]
             roofline["traffic"] = (j["dram_read_GB"] + j["dram_write_GB"]) * 1e9
-            roofline["traffic_source"] = "ncu dram__bytes_read+write per step, profiles/r01d_traffic_cfg5.json"
+            roofline["traffic_source"] = "ncu dram__bytes_read+write per step, profiles/r01k_traffic_cfg5.json"
         asm_b = sum(asm_bytes(l, c) for l, c in zip(layers, shares))
         hbm = peaks.get("hbm_gbs", 6650.0)
         k1_s = sum(k1) / args.steps
