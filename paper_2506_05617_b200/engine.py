@@ -283,13 +283,22 @@ def batched_svd_grouped(groups, dtype: str, want_vectors: bool, tol=DEFAULT_SVD_
     table = (_lib.SvdGroup * len(groups))()
     dev = groups[0].device
     rows = 1
-    for g, blk in enumerate(groups):
+    # the library forks groups onto streams in table order: the costliest
+    # (count * mr * nc^2) first, so the long large-block solves start while
+    # the SMs are free and the small ones fill in around them
+    def cost(blk):
         count, co, ci = blk.shape
-        o = alloc_svd_outputs(count, co, ci, dtype, want_vectors, dev)
-        outs.append(o)
-        table[g] = _lib.SvdGroup(ptr(blk), count, co, ci, ptr(o.sigma), ptr(o.U), ptr(o.V),
-                                 ptr(o.info), ptr(o.zero), effective_tol(tol, dtype, max(co, ci)))
+        return count * max(co, ci) * min(co, ci) ** 2
+    order = sorted(range(len(groups)), key=lambda g: -cost(groups[g]))
+    for blk in groups:
+        count, co, ci = blk.shape
+        outs.append(alloc_svd_outputs(count, co, ci, dtype, want_vectors, dev))
         rows = max(rows, co, ci)
+    for slot, g in enumerate(order):
+        blk, o = groups[g], outs[g]
+        count, co, ci = blk.shape
+        table[slot] = _lib.SvdGroup(ptr(blk), count, co, ci, ptr(o.sigma), ptr(o.U), ptr(o.V),
+                                    ptr(o.info), ptr(o.zero), effective_tol(tol, dtype, max(co, ci)))
     code = dtype_code(dtype)
     ws_bytes = lib.cs_batched_svd_grouped_workspace(table, len(groups), code, int(want_vectors))
     ws = WORKSPACE.get(dev, ws_bytes)
