@@ -20,7 +20,7 @@ LIBNAME = "libconvspectra_b200.so"
 LIBPATH = os.path.join(LIBDIR, LIBNAME)
 
 SOURCES = ["cs_api.cu", "cs_symbol.cu", "cs_jacobi.cu", "cs_jacobi_f32.cu", "cs_jacobi_f64.cu",
-           "cs_spectrum.cu", "cs_warm.cu",
+           "cs_spectrum.cu", "cs_warm.cu", "cs_tcb.cu",
            "cs_operator.cu", "cs_analysis.cu", "cs_fft.cu"]
 # cuFFT (the FFT comparison route only) from the CUDA toolkit of this image
 LINK_LIBS = ["-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]

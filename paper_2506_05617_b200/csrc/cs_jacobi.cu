@@ -254,6 +254,18 @@ static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     return plan_generic<T>(co, ci, wantv, 8, false, s);
 }
 
+// tensor-core blocked kernel (cs_tcb.cu): fp32, vectors, instantiated shapes
+bool tcb_supported(int mr, int nc, bool wantv);
+int tcb_dispatch(const JacArgs<float> &a, cudaStream_t st);
+// experiment switch, read once: CS_TCB=0 keeps the scalar panel kernel
+static bool tcb_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("CS_TCB");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <typename T>
 static int dispatch(const JacArgs<T> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {
     if constexpr (sizeof(T) == 4) return jacobi_dispatch_f32(a, wantv, st, dry, ncl);
@@ -313,6 +325,11 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
         if (ws_bytes < need || (!ws && need))
             return fail(CS_ENOMEM, "batched SVD: workspace too small (query cs_batched_svd_workspace)");
         a.scratch = (cplx_t<T> *)ws;
+    }
+    if constexpr (sizeof(T) == 4) {
+        // warm-started solves only: cold starts (large rotations in every early
+        // sweep) are faster on the scalar panel kernel
+        if (tcb_enabled() && a.initX && tcb_supported(a.s.mr, a.s.nc, wantv)) return tcb_dispatch(a, st);
     }
     return dispatch<T>(a, wantv, st, false, nullptr);
 }

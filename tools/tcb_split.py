@@ -1,0 +1,25 @@
+"""Per-phase cycle split of the tensor-core blocked kernel (CS_TCB_CLOCKS build):
+CS_LIBPATH=ab_libs/libtcbclk.so python tools/tcb_split.py [COUNT] [WARM]"""
+import ctypes, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_05617_b200 import _lib, configs  # noqa: E402
+from paper_2506_05617_b200.pipeline import lfa_device  # noqa: E402
+count = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+warm = (sys.argv[2] != "0") if len(sys.argv) > 2 else False
+dev = torch.device("cuda:0")
+layer = configs.WORKLOADS[5].layers[0]
+wd = torch.from_numpy(configs.layer_weights(layer)).to(dev)
+L = _lib.load()
+buf = (ctypes.c_ulonglong * 10)()
+lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
+L.cs_debug_tcb_cycles(buf, 1)
+res = lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
+L.cs_debug_tcb_cycles(buf, 0)
+n = buf[9]
+names = ["gram", "G-read", "angles", "D (rot/exp)", "bop+update", "epi-add", "exch-transfer", "exch-wait"]
+tot = sum(buf[i] for i in range(8))
+print(f"{count} blocks warm={warm}: {n} super-rounds on CTA thread 0s, sweeps {res.info.float().mean().item():.2f}")
+for i, nm in enumerate(names):
+    print(f"  {nm:12s} {buf[i] / n:8.0f} cycles/super-round ({100 * buf[i] / tot:.1f}%)")
+print(f"  total        {tot / n:8.0f}")
