@@ -53,7 +53,55 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the FFT-route / analysis timings")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the cpu_baseline / reference sample")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the timed fp64 (1e-10 mode) step")
+    ap.add_argument("--launcher-dry-run", action="store_true",
+                    help="test hook: spawn the ranks and run the rendezvous / max-over-ranks "
+                         "timing on gloo without a GPU (no hot path)")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: launch N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code.  Fails loudly
+    when fewer than N GPUs are visible (the dry-run test hook excepted)."""
+    if not args.launcher_dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} requested but {have} CUDA device(s) visible"}),
+                  flush=True)
+            return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def launcher_dry_run(args, rank, world):
+    """Rendezvous + timing reduction of the N-rank path on gloo (CPU test)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    try:
+        dist.barrier()
+        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(json.dumps({"metric": "launcher dry run", "n_gpus": world, "ranks_seen": world,
+                              "max_over_ranks": float(t.item()), "backend": dist.get_backend()}),
+                  flush=True)
+    finally:
+        dist.destroy_process_group()
 
 
 def host_threads() -> int:
@@ -246,6 +294,51 @@ def workload_config(wl, ngpu):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def fp64_step(wl, layer, w32, dev):
+    """One timed fp64 step (the 1e-10 parity mode, like-for-like with the
+    reference's complex128 arithmetic): K1 -> warm-started Jacobi with U, V ->
+    sort, in float64, device-timed, no warm-up.  Roofline against the DFMA
+    rate measured on this GPU; sampled parity against the reference's
+    golden sigma (tests/golden, made by the reference itself)."""
+    import torch
+
+    import paper_2506_05617_b200 as cs
+    from paper_2506_05617_b200 import engine
+
+    torch.cuda.empty_cache()
+    w64 = w32.double()
+    tm = engine.Timer(dev)
+    res = cs.lfa_device(w64, layer.n, layer.m, "f64", wl.vectors, timer=tm)
+    torch.cuda.synchronize(dev)
+    total = tm.seconds("t0", "t3")
+    svd_s = tm.seconds("t1", "t2")
+    info = res.info.cpu().numpy()
+    peak = engine.fma_peak_flops("f64", dev.index)
+    fl = svd_flops(layer, wl.vectors)
+    out = {"value": wl.sv_count / total, "unit": "singular values/s", "ms_per_step": 1e3 * total,
+           "svd_ms": 1e3 * svd_s, "sweeps_mean": float(info.mean()), "converged": bool((info > 0).all()),
+           "roofline": {"bound": "fp64", "achieved": fl / svd_s / 1e12, "peak": peak / 1e12,
+                        "unit": "TFLOP/s", "frac": fl / svd_s / peak,
+                        "peak_source": "cs_measure_fma_peak(CS_F64) on this GPU in this run",
+                        "algorithmic": "Golub-Reinsch count x4 complex per unique block (SURVEY 8(d))"},
+           "what": "one fp64 step, no warm-up (plans cached by the fp32 steps)"}
+    gpath = os.path.join(ROOT, "tests", "golden", "golden.npz")
+    key = f"{wl.name.split('_')[0]}_l0"
+    if os.path.exists(gpath):
+        g = np.load(gpath)
+        if key + "_sigma" in g.files:
+            rep_of, _ = engine.partner_map(layer.n, layer.m)
+            sig = res.sigma.cpu().numpy()[rep_of[g[key + "_fidx"]]]
+            ref = g[key + "_sigma"]
+            err = float((np.abs(sig - ref).max(axis=1) / ref[:, 0]).max())
+            out["parity"] = {"frequencies": int(len(ref)), "max_rel_err": err, "bar": 1e-10,
+                             "ok": err <= 1e-10,
+                             "reference": "tests/golden/golden.npz (the reference's own sigma)"}
+    del res
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, wl, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -331,15 +424,17 @@ def run_ours(args, wl, rank, world, local_rank):
         svd_flops_step = sum(svd_flops(l, wl.vectors, c) for l, c in zip(layers, shares))
         svd_s = sum(sv) / args.steps
         achieved = svd_flops_step / svd_s / 1e12
-        roofline = {"kernel": "jacobi_panel_kernel (K2/K3 batched one-sided Jacobi; SVD phase "
-                              "incl. warm-start GEMMs, summed over its launches)",
+        roofline = {"kernel": "SVD phase summed over its launches: jacobi_tcb_kernel (tensor-core "
+                              "blocked Jacobi, warm stages of 256x256+V) / jacobi_panel_kernel (seeds, "
+                              "other shapes) + warm-start GEMMs",
                     "bound": "fp32", "achieved": achieved, "peak": fma_peak / 1e12,
                     "unit": "TFLOP/s", "frac": achieved * 1e12 / fma_peak,
                     "traffic": None,
                     "peak_source": "measured on this GPU in this run (cs_measure_fma_peak: "
                                    "dependent-FFMA probe); MEASURED_PEAKS.json holds no FP32 peak",
-                    "algorithmic": "Golub-Reinsch sigma+U+V count x4 complex per unique block "
-                                   "(SURVEY 8(d)); Jacobi executes ~3.5x more"}
+                    "algorithmic": ("Golub-Reinsch sigma+U+V count x4 complex per unique block (SURVEY 8(d))"
+                                    if wl.vectors else
+                                    "Golub-Reinsch sigma-only count x4 complex per unique block (SURVEY 8(d))")}
         # DRAM traffic per step from the committed ncu capture of this workload
         # (profiles/r01k_traffic_cfg5.json; null for other workloads / N > 1)
         trf = {}
@@ -375,13 +470,14 @@ def run_ours(args, wl, rank, world, local_rank):
         for _ in range(args.e2e_steps):
             if len(layers) > 1 and world == 1:  # one batched call for all layers
                 res = cs.compute_spectra(kernels, [cs.SpatialDims(l.n, l.m) for l in layers],
-                                         values_only=not wl.vectors, device=dev)
+                                         values_only=not wl.vectors, device=dev, dtype="f32")
                 d2h += sum(r.values.nbytes for r in res)
                 continue
             for k, l in zip(kernels, layers):
                 dims = cs.SpatialDims(l.n, l.m)
                 if world == 1:
-                    res = cs.compute_spectrum(k, dims, values_only=not wl.vectors, device=dev)
+                    res = cs.compute_spectrum(k, dims, values_only=not wl.vectors, device=dev,
+                                              dtype="f32")
                     vals = res.values
                 else:
                     w = torch.from_numpy(k.device_weights("f32")).to(dev)
@@ -398,9 +494,10 @@ def run_ours(args, wl, rank, world, local_rank):
         e2e = {"value": svs * args.e2e_steps / el, "unit": "singular values/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.e2e_steps,
                "api": ("distributed.lfa_sharded (host weights in, sorted values out)" if world > 1
-                       else "paper_2506_05617_b200.compute_spectra(kernels, dims) (one batched call)"
+                       else "paper_2506_05617_b200.compute_spectra(kernels, dims, dtype='f32') (one batched call)"
                        if len(layers) > 1 else
-                       f"paper_2506_05617_b200.compute_spectrum(kernel, dims, values_only={not wl.vectors})")}
+                       f"paper_2506_05617_b200.compute_spectrum(kernel, dims, values_only={not wl.vectors}, "
+                       "dtype='f32')")}
 
     # SURVEY 8(f) rows measured next to the hot path (1 GPU, single layer):
     # the FFT route's assembly (the paper's comparison baseline) vs K1, and
@@ -437,8 +534,12 @@ def run_ours(args, wl, rank, world, local_rank):
                             "values": int(vals.numel()), "sigma_max": summ.sigma_max, "w1": w1},
         }
 
+    fp64 = None
+    if world == 1 and len(layers) == 1 and not args.no_fp64:
+        fp64 = fp64_step(wl, layers[0], w_dev[0], dev)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, host_threads(), args.cpu_seconds)
 
     # kernel launches of ours per step: per layer K1 + the SVD stages (cold seeds
@@ -473,6 +574,7 @@ def run_ours(args, wl, rank, world, local_rank):
             "roofline": roofline, "roofline_assembly": roofline_k1,
             "phases": phases, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "sweeps_mean": sweeps_mean, "converged": ok, "extras": extras,
+            "fp64": fp64,
             "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)
@@ -480,12 +582,18 @@ def run_ours(args, wl, rank, world, local_rank):
 
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     wl = configs.WORKLOADS[args.config]
-    if args.impl == "reference":
+    if args.impl == "reference":  # rank 0 alone times the CPU reference path
         run_reference(args, wl, rank)
+        return
+    if not launched and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if args.launcher_dry_run:
+        launcher_dry_run(args, rank, world)
         return
     if world > 1:
         import torch

@@ -106,6 +106,7 @@ def svd_block(block, k=None, tol=DEFAULT_SVD_TOL, max_sweeps=DEFAULT_MAX_SWEEPS,
     b = np.atleast_2d(np.asarray(block, dtype=np.complex128))
     dev = engine.require_cuda(device)
     dt = "f64" if dtype is None else _infer_dtype(b, dtype)
+    engine.check_tol(tol, dt, max(b.shape))
     t = _to_device_blocks(b[None], dev, dt)
     out = engine.batched_svd(t, dt, True, tol, max_sweeps)
     f = engine.first_failure(out.info)
@@ -142,9 +143,13 @@ def spectrum_from_field(fld, values_only: bool = True, workers: int = 1,
     half = full_grid and engine.is_conj_symmetric(t, n, m, dt)
     reps = engine.half_grid_indices(n, m) if half else None
 
+    engine.check_tol(tol, dt, max(co, ci))
     tm.mark("t0")
     work = t.index_select(0, torch.from_numpy(reps).to(dev)) if half else t
-    out = engine.batched_svd(work, dt, not values_only, tol, max_sweeps)
+    # values_only=True runs the vectors solve when that is the panel kernel, so
+    # values agree bitwise with values_only=False (blocksvd.py:4-8, T/test_blocksvd.py:110-116)
+    vec = (not values_only) or engine.values_via_vectors(work.shape[0], co, ci, dt)
+    out = engine.batched_svd(work, dt, vec, tol, max_sweeps)
     values_dev = engine.spectrum_values(out.sigma, dt, n, m, half)
     ffail = engine.first_failure(out.info)
     tm.mark("t1")

@@ -111,8 +111,14 @@ __device__ __forceinline__ void gram_stage(const unsigned char *P, uint32_t atom
         h.y = *reinterpret_cast<const float *>(P + sw_off(r0 + 4 * rq + 1, j, atom));
         h.z = *reinterpret_cast<const float *>(P + sw_off(r0 + 4 * rq + 2, j, atom));
         h.w = *reinterpret_cast<const float *>(P + sw_off(r0 + 4 * rq + 3, j, atom));
-        *reinterpret_cast<float4 *>(stg + sw_chunk(j, rq, 16384)) = h;
-        *reinterpret_cast<float4 *>(stg + sw_chunk(64 + j, rq, 16384)) = lo4(h);
+        // round-to-nearest split (hi symmetric around x): the dropped lo*lo
+        // term is then unbiased -- with the truncated hi it would be a
+        // systematic positive term on the diagonal
+        const float4 hr = make_float4(rna_tf32(h.x), rna_tf32(h.y), rna_tf32(h.z), rna_tf32(h.w));
+        const float4 lr = make_float4(rna_tf32(h.x - hr.x), rna_tf32(h.y - hr.y), rna_tf32(h.z - hr.z),
+                                      rna_tf32(h.w - hr.w));
+        *reinterpret_cast<float4 *>(stg + sw_chunk(j, rq, 16384)) = hr;
+        *reinterpret_cast<float4 *>(stg + sw_chunk(64 + j, rq, 16384)) = lr;
     }
 }
 
@@ -137,7 +143,11 @@ __device__ __forceinline__ void build_bop(const float2 *Dm, unsigned char *B) {
         const int x = threadIdx.x + e * NT, n = x >> 6, k = x & 63;
         const float2 dv = Dm[(k >> 1) * LDG + (n >> 1)];
         const float v = (n & 1) == 0 ? ((k & 1) == 0 ? dv.x : -dv.y) : ((k & 1) == 0 ? dv.y : dv.x);
-        const float h = trunc_tf32(v);
+        // round-to-nearest split of D: the panel's hi is the truncated word
+        // (lo(P) >= 0 relative to P), so the dropped lo(P) lo(D) term is
+        // unbiased only if lo(D) is symmetric -- a truncated split of D too
+        // shrank column norms by ~2e-6 per solve (measured, cfg5)
+        const float h = rna_tf32(v);
         *reinterpret_cast<float *>(B + sw_off(n, k, 16384)) = h;
         *reinterpret_cast<float *>(B + sw_off(64 + n, k, 16384)) = rna_tf32(v - h);
     }

@@ -73,6 +73,23 @@ def dtype_of_tensor(t) -> str:
 TOL32_FLOOR = 2.5e-6
 
 
+def check_tol(tol: float, dtype: str, rows: int) -> None:
+    """Warn when a caller-supplied tolerance cannot be honoured in fp32.
+
+    The reference default (1e-13, passed implicitly as DEFAULT_SVD_TOL) is
+    floored silently in fp32 mode; an explicit value below the fp32
+    resolution floor is floored too, but with a warning."""
+    if dtype != "f32" or tol is DEFAULT_SVD_TOL:
+        return
+    floor = TOL32_FLOOR * math.sqrt(max(rows, 1) / 64.0)
+    if float(tol) < floor:
+        import warnings
+
+        warnings.warn(f"tol={tol:g} is below the fp32 resolution floor {floor:.3g} for {rows}-row "
+                      f"blocks; the fp32 solve uses {floor:.3g} (pass dtype='f64' for tighter "
+                      "tolerances)", RuntimeWarning, stacklevel=3)
+
+
 def effective_tol(tol: float, dtype: str, rows: int) -> float:
     """Convergence threshold actually used by the kernel.
 
@@ -97,7 +114,10 @@ def ptr(t) -> int:
 
 
 class _Workspace:
-    """Grow-only device scratch per device (the C-ABI owns no memory)."""
+    """Grow-only device scratch per (device, stream) (the C-ABI owns no
+    memory).  Keyed by the current stream so solves on different streams never
+    share scratch; growth frees the old buffer through the caching allocator,
+    which is stream-ordered on that same stream."""
 
     def __init__(self):
         self._buf = {}
@@ -105,7 +125,7 @@ class _Workspace:
     def get(self, device, nbytes: int):
         if nbytes <= 0:
             return None
-        key = (device.type, device.index)
+        key = (device.type, device.index, torch.cuda.current_stream(device).cuda_stream)
         buf = self._buf.get(key)
         if buf is None or buf.numel() < nbytes:
             self._buf[key] = None
@@ -455,6 +475,15 @@ def use_warm_start(count: int, co: int, ci: int, dtype: str, want_vectors: bool,
     if not requested or count < 3:
         return False
     return plan_kind(count, co, ci, dtype, True) == 2
+
+
+def values_via_vectors(count: int, co: int, ci: int, dtype: str) -> bool:
+    """Whether a values-only drop-in call runs the vectors solve (factors
+    dropped): yes whenever the vectors solve is the panel / tensor-core
+    kernel, so values_only=True and False agree bit for bit.  Shapes whose
+    vectors solve needs the generic fallback kernel keep the faster
+    values-only kernel (values then agree to fp rounding, not bitwise)."""
+    return count > 0 and plan_kind(count, co, ci, dtype, True) == 2
 
 
 def use_warm_values(count: int, co: int, ci: int, dtype: str) -> bool:

@@ -119,12 +119,11 @@ def compute_spectra(kernels, dims, values_only: bool = True, tol: float = DEFAUL
     kernels = list(kernels)
     dims_l = list(dims) if isinstance(dims, (list, tuple)) else [dims] * len(kernels)
     dev = engine.require_cuda(device)
-    dts = {_resolve_dtype(k, dtype) for k in kernels}
-    if len(dts) != 1:
-        raise ValueError("compute_spectra: all kernels must share one precision (pass dtype=)")
-    dt = dts.pop()
+    dt = _resolve_dtype(kernels[0] if kernels else None, dtype)
     for k in kernels:
         validate_kernel(k)
+    for k in kernels:
+        engine.check_tol(tol, dt, max(k.c_out, k.c_in))
     layers = [(engine.weights_to_device(k, dt, dev), d.n, d.m) for k, d in zip(kernels, dims_l)]
     tm = engine.Timer(dev)
     outs = lfa_device_multi(layers, dt, not values_only, tol, max_sweeps, timer=tm)
@@ -179,14 +178,21 @@ def compute_spectrum(kernel: ConvKernel, dims: SpatialDims, method: str = "lfa",
     dt = _resolve_dtype(kernel, dtype)
     n, m = dims.n, dims.m
     co, ci = kernel.c_out, kernel.c_in
-    need = field_bytes((co, ci), n, m, dt, not values_only)
+    engine.check_tol(tol, dt, max(co, ci))
+    # values_only=True runs the same solve as values_only=False whenever that
+    # solve is the panel / tensor-core kernel, so the two return bitwise equal
+    # values (the reference's guarantee, pipeline.py:40-42); the factors are
+    # computed and dropped
+    vec = (not values_only) or engine.values_via_vectors(engine.half_grid_count(n, m), co, ci, dt)
+    need = field_bytes((co, ci), n, m, dt, vec)
     if method == "fft":  # plus the embedded channel-pair grids (fft.py:123-130)
         need += co * ci * n * m * (8 if dt == "f32" else 16)
     engine.check_budget(need, engine.device_budget_bytes(dev, mem_budget_gib),
                         f"{method.upper()} solve ({engine.half_grid_count(n, m)} blocks of {co}x{ci})")
     w = engine.weights_to_device(kernel, dt, dev)
     tm = engine.Timer(dev)
-    res = lfa_device(w, n, m, dt, not values_only, tol, max_sweeps, timer=tm, method=method)
+    res = lfa_device(w, n, m, dt, vec, tol, max_sweeps, timer=tm, method=method)
+    res.U = res.V = None  # compute_spectrum returns values only (pipeline.py:69)
     f = engine.first_failure(res.info)
     if f >= 0:
         reps = engine.half_grid_indices(n, m)

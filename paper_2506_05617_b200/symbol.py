@@ -63,8 +63,12 @@ class SymbolField:
 
 
 def _resolve_dtype(kernel: ConvKernel, dtype) -> str:
+    """Compute precision.  The reference computes in float64 whatever the
+    weights' precision tag (kernels.py:40, symbol.py:134), so the drop-in does
+    too; fp32 (the measured complex64 mode, 1e-5 of sigma_max per frequency)
+    is an explicit opt-in with dtype="f32"."""
     if dtype is None:
-        return kernel.precision
+        return "f64"
     if dtype in ("f32", "float32", "complex64"):
         return "f32"
     if dtype in ("f64", "float64", "complex128"):

@@ -38,3 +38,21 @@ def test_our_arm_contract(cuda):
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
+
+
+def test_gpus_flag_spawns_ranks():
+    """--gpus N without torchrun launches N ranks (torch.distributed.run on
+    127.0.0.1); the launcher hook checks the rendezvous and the max-over-ranks
+    reduction on gloo (no GPU needed)."""
+    d = _run(["--gpus", "2", "--launcher-dry-run"], 600)
+    assert d["n_gpus"] == 2 and d["ranks_seen"] == 2 and d["max_over_ranks"] == 2.0
+
+
+def test_gpus_flag_fails_loudly_without_gpus():
+    """Asking for more GPUs than are visible is an error, not a silent 1-GPU run."""
+    import torch
+
+    n = torch.cuda.device_count() + 1
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(max(n, 2)),
+                          "--config", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode != 0 and "visible" in out.stdout

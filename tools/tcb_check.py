@@ -23,7 +23,12 @@ torch.cuda.synchronize()
 t_svd = min(t_svd, tm.seconds("t1", "t2"))
 sig = res.sigma.cpu().numpy()
 info = res.info.cpu().numpy()
+Aall = engine.symbol_field(wd, layer.n, layer.m, "f32", half=True, f_first=0, f_count=count)
+fro = (Aall.abs().double() ** 2).sum(dim=(1, 2)).cpu().numpy()
+del Aall
+en = (np.sum(sig.astype(np.float64) ** 2, axis=1) - fro) / fro
 out = {"count": count, "warm": warm, "tcb": os.environ.get("CS_TCB", "1"), "svd_ms": 1e3 * t_svd,
+       "energy_bias": float(en.mean()), "energy_maxabs": float(np.abs(en).max()),
        "sweeps_mean": float(info.mean()), "sweeps_max": int(info.max()), "failed": int((info <= 0).sum())}
 U = res.U[: min(count, 8)].cpu().numpy().astype(np.complex128)
 V = res.V[: min(count, 8)].cpu().numpy().astype(np.complex128)
