@@ -345,7 +345,7 @@ def run_ours(args, wl, rank, world, local_rank):
 
     import paper_2506_05617_b200 as cs
     from paper_2506_05617_b200 import engine
-    from paper_2506_05617_b200.distributed import lfa_sharded, shard_range
+    from paper_2506_05617_b200.distributed import lfa_sharded, shard_ids
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -419,8 +419,7 @@ def run_ours(args, wl, rank, world, local_rank):
         phases = {"assembly_K1_ms": 1e3 * sum(k1) / args.steps,
                   "svd_ms": 1e3 * sum(sv) / args.steps,
                   "spectrum_sort_ms": 1e3 * sum(asm) / args.steps}
-        shares = [(shard_range(half_count(l.n, l.m), rank, world)[1] if world > 1 else None)
-                  for l in layers]
+        shares = [(len(shard_ids(l.n, l.m, rank, world)) if world > 1 else None) for l in layers]
         svd_flops_step = sum(svd_flops(l, wl.vectors, c) for l, c in zip(layers, shares))
         svd_s = sum(sv) / args.steps
         achieved = svd_flops_step / svd_s / 1e12
@@ -549,10 +548,10 @@ def run_ours(args, wl, rank, world, local_rank):
     per_step = 0
     for l in (layers if not (len(layers) > 1 and world == 1) else []):
         total = half_count(l.n, l.m)
-        u0, cnt = (0, total) if world == 1 else shard_range(total, rank, world)
-        if (engine.use_warm_start(cnt, l.c_out, l.c_in, dt, wl.vectors) or
-                (not wl.vectors and engine.use_warm_values(cnt, l.c_out, l.c_in, dt))):
-            stages = len(engine.warm_plan(l.n, l.m, u0, cnt, dev, engine.warm_depth(cnt)))
+        ids = np.arange(total) if world == 1 else shard_ids(l.n, l.m, rank, world)
+        if (engine.use_warm_start(total, l.c_out, l.c_in, dt, wl.vectors) or
+                (not wl.vectors and engine.use_warm_values(total, l.c_out, l.c_in, dt))):
+            stages = len(engine.subset_plan(l.n, l.m, ids, "cpu"))
             per_step += 1 + stages + (stages - 1) + 1
         else:
             per_step += 1 + 1 + (1 if wl.vectors else 0)

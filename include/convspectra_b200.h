@@ -104,11 +104,17 @@ int cs_batched_svd_plan_kind(int dtype, long long count, int c_out, int c_in,
  * init_X it starts from X = init_X[i] ((mr, nc) row-major, working
  * orientation X = A or A^H) instead of the block, and with init_V from
  * V = init_V[init_V_index[i]] ((nc, nc) row-major) instead of the identity.
- * Same algorithm, tolerance and outputs as cs_batched_svd. */
+ * Same algorithm, tolerance and outputs as cs_batched_svd.  index may be NULL
+ * (item i solves matrix i).  plan_count > 0 makes the kernel configuration
+ * (cluster size, panel width -- hence the rotation order and the result bits)
+ * that of a batch of plan_count matrices, independent of `count`: a frequency
+ * shard then reproduces the single-GPU solve bit for bit (the reference's
+ * partition guarantee, blocksvd.py:4-8); <= 0 plans for `count`. */
 int cs_batched_svd_indexed(const void *blocks, int dtype, long long count, int c_out,
                            int c_in, int want_vectors, double tol, int max_sweeps,
                            const long long *index, const void *init_X, const void *init_V,
-                           const long long *init_V_index, void *sigma, void *U, void *V,
+                           const long long *init_V_index, long long plan_count, void *sigma,
+                           void *U, void *V,
                            int *info, int *zero_sigma, void *workspace,
                            size_t workspace_bytes, void *stream);
 

@@ -48,8 +48,8 @@ _SIGNATURES = {
     "cs_batched_svd": (_i, [_vp, _i, _ll, _i, _i, _i, _d, _i, _vp, _vp, _vp, _vp, _vp, _vp,
                             _sz, _vp]),
     "cs_batched_svd_plan_kind": (_i, [_i, _ll, _i, _i, _i]),
-    "cs_batched_svd_indexed": (_i, [_vp, _i, _ll, _i, _i, _i, _d, _i, _vp, _vp, _vp, _vp, _vp,
-                                    _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "cs_batched_svd_indexed": (_i, [_vp, _i, _ll, _i, _i, _i, _d, _i, _vp, _vp, _vp, _vp, _ll,
+                                    _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "cs_warm_start_gemm": (_i, [_vp, _i, _i, _i, _ll, _vp, _vp, _vp, _vp, _vp]),
     "cs_batched_svd_grouped_workspace": (_sz, [ctypes.POINTER(SvdGroup), _i, _i, _i]),
     "cs_batched_svd_grouped": (_i, [ctypes.POINTER(SvdGroup), _i, _i, _i, _d, _i, _vp, _sz,

@@ -164,23 +164,60 @@ def spectrum_from_field(fld, values_only: bool = True, workers: int = 1,
                             device_values=values_dev if return_device_tensors else None)
     if values_only:
         return result
-    sig, U, V = out.sigma, out.U, out.V
-    if half:
-        U = engine.expand_half(U, n, m, dt)
-        V = engine.expand_half(V, n, m, dt)
-        rep_of, _ = engine.partner_map(n, m)
-        sig = sig.index_select(0, torch.from_numpy(rep_of).to(dev))
-    freqs = grid.frequencies
-    if return_device_tensors:
-        trip = [SvdTriplet(k=(freqs[f, 0], freqs[f, 1]), U=U[f], sigma=sig[f], V=V[f])
-                for f in range(F)]
-        return result, trip
-    Uh = U.cpu().numpy().astype(np.complex128)
-    Vh = V.cpu().numpy().astype(np.complex128)
-    Sh = sig.cpu().numpy().astype(np.float64)
-    trip = [SvdTriplet(k=(freqs[f, 0], freqs[f, 1]), U=Uh[f], sigma=Sh[f], V=Vh[f])
-            for f in range(F)]
+    trip = TripletList(out.sigma, out.U, out.V, grid.frequencies, n, m, half,
+                       host=not return_device_tensors)
     return result, trip
+
+
+class TripletList:
+    """Per-frequency triplets in grid order, materialised on access.
+
+    The reference returns a list whose U/V are views into shared batch
+    arrays (blocksvd.py:271-275).  Here the factors stay on the device at
+    their solved size: for a conjugate-symmetric field only the
+    representatives are stored and the partner f* of a representative u gets
+    U_f* = conj(U_u), V_f* = conj(V_u), sigma_f* = sigma_u -- the
+    full cfg5 grid (2 x 34 GB of fp32 factors expanded, 2 x 69 GB as host
+    complex128) is never built.  Item access returns an SvdTriplet with host
+    complex128 / float64 arrays (host=True, the reference's types) or device
+    tensors; indexing, iteration, len() and slices work like the list."""
+
+    def __init__(self, sigma, U, V, freqs, n, m, half, host=True):
+        self._sig, self._U, self._V = sigma, U, V
+        self._freqs = freqs
+        self._host = host
+        self._n = len(freqs)
+        if half:
+            rep_of, conj = engine.partner_map(n, m)
+            self._rep, self._conj = rep_of, conj
+        else:
+            self._rep, self._conj = np.arange(self._n), np.zeros(self._n, dtype=bool)
+
+    def __len__(self):
+        return self._n
+
+    def __iter__(self):
+        for f in range(self._n):
+            yield self[f]
+
+    def __getitem__(self, f):
+        if isinstance(f, slice):
+            return [self[i] for i in range(*f.indices(self._n))]
+        f = int(f)
+        if f < 0:
+            f += self._n
+        if not 0 <= f < self._n:
+            raise IndexError(f"frequency index {f} out of range for {self._n} frequencies")
+        u, cj = int(self._rep[f]), bool(self._conj[f])
+        Uf, Vf, sf = self._U[u], self._V[u], self._sig[u]
+        if cj:
+            Uf, Vf = Uf.conj(), Vf.conj()
+        if self._host:
+            Uf = Uf.resolve_conj().cpu().numpy().astype(np.complex128)
+            Vf = Vf.resolve_conj().cpu().numpy().astype(np.complex128)
+            sf = sf.cpu().numpy().astype(np.float64)
+        k = (self._freqs[f, 0], self._freqs[f, 1])
+        return SvdTriplet(k=k, U=Uf, sigma=sf, V=Vf)
 
 
 def engine_timings(fld, s_svd: float) -> PhaseTimings:

@@ -294,10 +294,11 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
                    int max_sweeps, void *sigma, void *U, void *V, int *info, int *zero_sigma,
                    void *ws, size_t ws_bytes, cudaStream_t st, const long long *index = nullptr,
                    const void *initX = nullptr, const void *initV = nullptr,
-                   const long long *initV_index = nullptr) {
+                   const long long *initV_index = nullptr, long long plan_count = 0) {
     if (count == 0) return CS_OK;
     JacArgs<T> a = {};
-    if (!plan<T>(co, ci, wantv, count, a.s)) return fail(CS_EINVAL, "batched SVD: no plan");
+    if (!plan<T>(co, ci, wantv, plan_count > 0 ? plan_count : count, a.s))
+        return fail(CS_EINVAL, "batched SVD: no plan");
     if ((index || initX || initV) && a.s.kind != 2)
         return fail(CS_EINVAL, "batched SVD: indexed / warm-started solves need the panel kernel");
     if (initV && !(wantv && initV_index)) return fail(CS_EINVAL, "batched SVD: initV needs vectors and an index");
@@ -320,7 +321,7 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
     a.Vw = (cplx_t<T> *)(a.s.wide ? U : V);
     if (!a.s.smem_resident) {
         size_t need = 0;
-        int stt = svd_workspace<T>(count, co, ci, wantv, &need);
+        int stt = svd_workspace<T>(plan_count > 0 ? std::max(count, plan_count) : count, co, ci, wantv, &need);
         if (stt) return stt;
         if (ws_bytes < need || (!ws && need))
             return fail(CS_ENOMEM, "batched SVD: workspace too small (query cs_batched_svd_workspace)");
@@ -386,7 +387,8 @@ extern "C" int cs_batched_svd_indexed(const void *blocks, int dtype, long long c
                                       int c_in, int want_vectors, double tol, int max_sweeps,
                                       const long long *index, const void *init_X,
                                       const void *init_V, const long long *init_V_index,
-                                      void *sigma, void *U, void *V, int *info, int *zero_sigma,
+                                      long long plan_count, void *sigma, void *U, void *V,
+                                      int *info, int *zero_sigma,
                                       void *workspace, size_t workspace_bytes, void *stream) {
     int st = check_svd_args(dtype, count, c_out, c_in, max_sweeps);
     if (st) return st;
@@ -398,10 +400,10 @@ extern "C" int cs_batched_svd_indexed(const void *blocks, int dtype, long long c
     if (dtype == CS_F32)
         return svd_run<float>(blocks, count, c_out, c_in, wv, tol, max_sweeps, sigma, U, V, info,
                               zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream, index,
-                              init_X, init_V, init_V_index);
+                              init_X, init_V, init_V_index, plan_count);
     return svd_run<double>(blocks, count, c_out, c_in, wv, tol, max_sweeps, sigma, U, V, info,
                            zero_sigma, workspace, workspace_bytes, (cudaStream_t)stream, index,
-                           init_X, init_V, init_V_index);
+                           init_X, init_V, init_V_index, plan_count);
 }
 
 extern "C" size_t cs_batched_svd_grouped_workspace(const cs_svd_group *groups, int num_groups,

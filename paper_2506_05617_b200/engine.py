@@ -339,21 +339,23 @@ def plan_kind(count: int, co: int, ci: int, dtype: str, want_vectors: bool) -> i
 
 def batched_svd_indexed(blocks, dtype: str, want_vectors: bool, index, out: SvdBatch,
                         tol=DEFAULT_SVD_TOL, max_sweeps=DEFAULT_MAX_SWEEPS, init_X=None,
-                        init_V=None, init_V_index=None):
-    """Solve blocks[index[i]] (outputs at index[i]); optional warm start from
-    init_X[i] / init_V[init_V_index[i]] (cs_batched_svd_indexed)."""
+                        init_V=None, init_V_index=None, plan_count: int = 0):
+    """Solve blocks[index[i]] (outputs at index[i]; index None: all blocks);
+    optional warm start from init_X[i] / init_V[init_V_index[i]]
+    (cs_batched_svd_indexed).  plan_count > 0 fixes the kernel configuration
+    to that of a plan_count-matrix batch (shard-independent results)."""
     _, co, ci = blocks.shape
-    count = index.shape[0]
+    count = index.shape[0] if index is not None else blocks.shape[0]
     dev = blocks.device
     lib = _lib.load()
     code = dtype_code(dtype)
-    ws_bytes = lib.cs_batched_svd_workspace(code, count, co, ci, int(want_vectors))
+    ws_bytes = lib.cs_batched_svd_workspace(code, max(count, int(plan_count)), co, ci, int(want_vectors))
     ws = WORKSPACE.get(dev, ws_bytes)
     etol = effective_tol(tol, dtype, max(co, ci))
     st = lib.cs_batched_svd_indexed(ptr(blocks), code, count, co, ci, int(want_vectors), etol,
                                     int(max_sweeps), ptr(index), ptr(init_X), ptr(init_V),
-                                    ptr(init_V_index), ptr(out.sigma), ptr(out.U), ptr(out.V),
-                                    ptr(out.info), ptr(out.zero), ptr(ws), ws_bytes,
+                                    ptr(init_V_index), int(plan_count), ptr(out.sigma), ptr(out.U),
+                                    ptr(out.V), ptr(out.info), ptr(out.zero), ptr(ws), ws_bytes,
                                     stream_ptr(dev))
     _lib.check(st, "cs_batched_svd_indexed")
     return out
@@ -387,21 +389,9 @@ def warm_depth(count: int) -> int:
 WARM_DEPTH = int(_WARM_DEPTH_ENV) if _WARM_DEPTH_ENV is not None else 3  # warm_plan() default (no block shape)
 
 
-def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = None):
-    """Stages of a warm-started solve over representatives [u0, u0+count).
-
-    Representatives are nodes of the frequency lattice (i, j); two are
-    neighbours when they differ by one grid step in i or j (their symbols
-    differ by O(2 pi/n) relative).  Cold seeds sit on a (2*depth+1)-periodic
-    lattice; a breadth-first search from the seeds assigns every other
-    representative to the stage equal to its lattice distance, warm-started
-    from its BFS parent (solved one stage earlier).  Representatives not
-    reachable within the range become seeds.  Returns [(ids, pred_or_None)]
-    per stage as device int64 tensors of local indices."""
-    depth = WARM_DEPTH if depth is None else depth
-    key = (n, m, u0, count, str(device), depth)
-    if key in _WARM_PLANS:
-        return _WARM_PLANS[key]
+def _bfs_forest(n: int, m: int, u0: int, count: int, depth: int):
+    """Host BFS forest over representatives [u0, u0+count): (level, parent)
+    with parent as a local index (-1 for seeds)."""
     reps = half_grid_indices(n, m)[u0:u0 + count]
     ii, jj = reps // m, reps % m
     local = {(int(a), int(b)): q for q, (a, b) in enumerate(zip(ii, jj))}
@@ -430,6 +420,46 @@ def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = N
             break
         level[left[0]] = 0
         frontier = [int(left[0])]
+    return level, parent
+
+
+_FORESTS = {}
+
+
+def warm_forest(n: int, m: int, depth: int | None = None):
+    """The warm-start forest over ALL representatives of an n x m grid:
+    (level, parent, root) per representative (global indices).  A frequency
+    shard made of whole trees solves every block exactly as the single-GPU
+    plan does (same seed, same parent chain)."""
+    total = half_grid_count(n, m)
+    depth = warm_depth(total) if depth is None else depth
+    key = (n, m, depth)
+    if key not in _FORESTS:
+        level, parent = _bfs_forest(n, m, 0, total, depth)
+        root = np.arange(total, dtype=np.int64)
+        for q in np.argsort(level, kind="stable"):  # parents sit one level earlier
+            if parent[q] >= 0:
+                root[q] = root[parent[q]]
+        _FORESTS[key] = (level, parent, root)
+    return _FORESTS[key]
+
+
+def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = None):
+    """Stages of a warm-started solve over representatives [u0, u0+count).
+
+    Representatives are nodes of the frequency lattice (i, j); two are
+    neighbours when they differ by one grid step in i or j (their symbols
+    differ by O(2 pi/n) relatively).  Cold seeds sit on a (2*depth+1)-periodic
+    lattice; a breadth-first search from the seeds assigns every other
+    representative to the stage equal to its lattice distance, warm-started
+    from its BFS parent (solved one stage earlier).  Representatives not
+    reachable within the range become seeds.  Returns [(ids, pred_or_None)]
+    per stage as device int64 tensors of local indices."""
+    depth = WARM_DEPTH if depth is None else depth
+    key = (n, m, u0, count, str(device), depth)
+    if key in _WARM_PLANS:
+        return _WARM_PLANS[key]
+    level, parent = _bfs_forest(n, m, u0, count, depth)
     t = lambda x: torch.tensor(np.asarray(x, dtype=np.int64), device=device)
     plan = []
     for d in range(int(level.max()) + 1):
@@ -440,27 +470,62 @@ def warm_plan(n: int, m: int, u0: int, count: int, device, depth: int | None = N
     return plan
 
 
+def subset_plan(n: int, m: int, ids, device, depth: int | None = None):
+    """Stages of the global warm forest restricted to the representatives
+    `ids` (sorted; whole trees): [(local ids, local parents or None, global
+    stage size)].  The global stage size is the plan_count that keeps each
+    stage's kernel configuration that of the single-GPU solve."""
+    level, parent, _ = warm_forest(n, m, depth)
+    ids = np.asarray(ids, dtype=np.int64)
+    pos = np.full(len(level), -1, dtype=np.int64)
+    pos[ids] = np.arange(len(ids))
+    lv = level[ids]
+    t = lambda x: torch.tensor(np.asarray(x, dtype=np.int64), device=device)
+    plan = []
+    for d in range(int(level.max()) + 1):
+        sel = np.nonzero(lv == d)[0]
+        if len(sel) == 0:
+            continue
+        gsize = int(np.count_nonzero(level == d))
+        if d == 0:
+            plan.append((t(sel), None, gsize))
+        else:
+            par = pos[parent[ids[sel]]]
+            if (par < 0).any():
+                raise ValueError("a shard must consist of whole warm-start trees")
+            plan.append((t(sel), t(par), gsize))
+    return plan
+
+
 def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SVD_TOL,
-                     max_sweeps=DEFAULT_MAX_SWEEPS, depth: int | None = None):
-    """All blocks of a representative range; every non-seed block is
-    warm-started from its solved neighbour's right factor
-    (cs_warm_start_gemm + cs_batched_svd_indexed), stage by stage."""
+                     max_sweeps=DEFAULT_MAX_SWEEPS, depth: int | None = None, ids=None):
+    """All blocks of a representative range (or of the representative set
+    `ids` -- whole warm-start trees -- with `blocks` in that order); every
+    non-seed block is warm-started from its solved neighbour's right factor
+    (cs_warm_start_gemm + cs_batched_svd_indexed), stage by stage.  Each
+    stage is planned for its size in the whole grid's forest, so a shard's
+    blocks come out bit for bit as in the single-GPU solve."""
     count, co, ci = blocks.shape
     dev = blocks.device
-    if depth is None:
-        depth = warm_depth(count)
+    if ids is not None or u0 == 0 and count == half_grid_count(n, m):
+        sel_ids = np.arange(count) if ids is None else ids
+        stages = subset_plan(n, m, sel_ids, dev, depth)
+    else:
+        if depth is None:
+            depth = warm_depth(count)
+        stages = [(i, p, 0) for i, p in warm_plan(n, m, u0, count, dev, depth)]
     out = alloc_svd_outputs(count, co, ci, dtype, True, dev)
     wide = co < ci
     mr, nc = (ci, co) if wide else (co, ci)
     Vw = out.U if wide else out.V
-    for ids, pred in warm_plan(n, m, u0, count, dev, depth):
+    for sel, pred, gsize in stages:
         if pred is None:
-            batched_svd_indexed(blocks, dtype, True, ids, out, tol, max_sweeps)
+            batched_svd_indexed(blocks, dtype, True, sel, out, tol, max_sweeps, plan_count=gsize)
         else:
-            Xw = torch.empty((ids.shape[0], mr, nc), dtype=blocks.dtype, device=dev)
-            warm_start_gemm(blocks, dtype, ids, pred, Vw, Xw)
-            batched_svd_indexed(blocks, dtype, True, ids, out, tol, max_sweeps, init_X=Xw,
-                                init_V=Vw, init_V_index=pred)
+            Xw = torch.empty((sel.shape[0], mr, nc), dtype=blocks.dtype, device=dev)
+            warm_start_gemm(blocks, dtype, sel, pred, Vw, Xw)
+            batched_svd_indexed(blocks, dtype, True, sel, out, tol, max_sweeps, init_X=Xw,
+                                init_V=Vw, init_V_index=pred, plan_count=gsize)
             del Xw
     complete_zero_columns(out, co, ci, dtype)
     return out

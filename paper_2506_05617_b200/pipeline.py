@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import engine
 from .blocksvd import PhaseTimings, SpectrumResult, resolve_workers
 from .engine import DEFAULT_MAX_SWEEPS, DEFAULT_SVD_TOL
@@ -39,20 +41,27 @@ class DeviceSpectrum:
     u0: int
     count: int
     dtype: str
+    ids: object = None      # representative indices of the rows (shards), or None: u0 + arange
 
 
 def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
                tol: float = DEFAULT_SVD_TOL, max_sweeps: int = DEFAULT_MAX_SWEEPS,
                u0: int = 0, count: int | None = None, assemble: bool = True,
                timer: engine.Timer | None = None, field_out=None,
-               warm_start=None, method: str = "lfa") -> DeviceSpectrum:
+               warm_start=None, method: str = "lfa", ids=None) -> DeviceSpectrum:
     """K1 -> K2/K3 -> assembly on the current stream, no host synchronisation.
 
-    ``warm_start`` (default: when vectors are requested and the panel kernel
-    applies) solves frequency triples [warm, seed, warm]: the seed cold, its
-    two grid neighbours from X A V_seed, which needs ~half the sweeps."""
+    Solves the representatives [u0, u0+count), or the representative set
+    ``ids`` (sorted; whole warm-start trees, distributed.shard_ids) -- then
+    every block is solved exactly as in the whole-grid solve, so shards
+    reproduce it bit for bit.  ``warm_start`` (default: when vectors are
+    requested and the panel kernel applies) solves each block of the
+    warm-start forest from its solved lattice neighbour's right factor."""
     total = engine.half_grid_count(n, m)
-    if count is None:
+    if ids is not None:
+        ids = np.asarray(ids, dtype=np.int64)
+        u0, count = int(ids[0]), len(ids)
+    elif count is None:
         count = total - u0
     if timer:
         timer.mark("t0")
@@ -60,17 +69,29 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
         if u0 != 0 or count != total:
             raise ValueError("the FFT route builds the whole half grid (u0=0, count=None)")
         fld = engine.fft_symbol_field(w_dev, n, m, dtype, half=True, timer=timer, out=field_out)
+    elif ids is not None:  # K1 over the covering range, then the shard's blocks
+        span = int(ids[-1]) - u0 + 1
+        rng = engine.symbol_field(w_dev, n, m, dtype, half=True, f_first=u0, f_count=span)
+        fld = rng if span == count else rng.index_select(0, torch_ids(ids - u0, w_dev.device))
+        del rng
     else:
         fld = engine.symbol_field(w_dev, n, m, dtype, half=True, f_first=u0, f_count=count,
                                   out=field_out)
     if timer:
         timer.mark("t1")
     co, ci = w_dev.shape[0], w_dev.shape[1]
-    if (engine.use_warm_start(count, co, ci, dtype, want_vectors, warm_start) or
-            (not want_vectors and warm_start is None and engine.use_warm_values(count, co, ci, dtype))):
-        out = engine.batched_svd_warm(fld, dtype, n, m, u0, tol, max_sweeps)
+    decide = total if ids is not None else count  # shards decide as the whole grid does
+    if (engine.use_warm_start(decide, co, ci, dtype, want_vectors, warm_start) or
+            (not want_vectors and warm_start is None and engine.use_warm_values(decide, co, ci, dtype))):
+        out = engine.batched_svd_warm(fld, dtype, n, m, u0, tol, max_sweeps, ids=ids)
         if not want_vectors:
             out.U = out.V = None
+    elif ids is not None:  # cold, planned as the whole grid
+        out = engine.alloc_svd_outputs(count, co, ci, dtype, want_vectors, fld.device)
+        engine.batched_svd_indexed(fld, dtype, want_vectors, None, out, tol, max_sweeps,
+                                   plan_count=total)
+        if want_vectors:
+            engine.complete_zero_columns(out, co, ci, dtype)
     else:
         out = engine.batched_svd(fld, dtype, want_vectors, tol, max_sweeps)
     if timer:
@@ -80,7 +101,11 @@ def lfa_device(w_dev, n: int, m: int, dtype: str, want_vectors: bool = False,
         values = engine.spectrum_values(out.sigma, dtype, n, m, True)
     if timer:
         timer.mark("t3")
-    return DeviceSpectrum(values, out.sigma, out.U, out.V, out.info, u0, count, dtype)
+    return DeviceSpectrum(values, out.sigma, out.U, out.V, out.info, u0, count, dtype, ids)
+
+
+def torch_ids(ids, device):
+    return engine.torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64)).to(device)
 
 
 def lfa_device_multi(layers, dtype: str, want_vectors: bool = False,

@@ -14,7 +14,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2506_05617_b200 import engine
-from paper_2506_05617_b200.distributed import gather_factors, gather_sigma, shard_range
+from paper_2506_05617_b200.distributed import gather_factors, gather_sigma, shard_ids, shard_range
 
 
 @pytest.mark.parametrize("total", [1, 7, 514, 32770])
@@ -42,11 +42,10 @@ def _worker(rank, world, port, n, m, r, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     total = engine.half_grid_count(n, m)
-    u0, cnt = shard_range(total, rank, world)
+    ids = shard_ids(n, m, rank, world)
     # each rank "solves" its representatives: sigma row u = [u, u/2, ...]
-    sig = torch.stack([torch.arange(u0, u0 + cnt, dtype=torch.float64) / (j + 1)
-                       for j in range(r)], dim=1)
-    full = gather_sigma(sig, total)
+    sig = torch.stack([torch.as_tensor(ids, dtype=torch.float64) / (j + 1) for j in range(r)], dim=1)
+    full = gather_sigma(sig, ids, total)
     if rank == 0:
         q.put(full.numpy())
     dist.destroy_process_group()
@@ -77,17 +76,42 @@ def _factor_worker(rank, world, port, total, rows, r, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    u0, cnt = shard_range(total, rank, world)
+    ids = np.array([u for u in range(total) if u % world == rank], dtype=np.int64)  # any row set
+    cnt = len(ids)
     # shard u of the factor: entries u + 1j * (row * r + col)
-    idx = torch.arange(u0, u0 + cnt, dtype=torch.float32)[:, None, None]
+    idx = torch.as_tensor(ids, dtype=torch.float32)[:, None, None]
     im = torch.arange(rows * r, dtype=torch.float32).reshape(1, rows, r)
     shard = torch.complex(idx.expand(cnt, rows, r), im.expand(cnt, rows, r)).contiguous()
-    full = gather_factors(shard, total, dst=world - 1)
+    full = gather_factors(shard, ids, total, dst=world - 1)
     if rank == world - 1:
         q.put(full.numpy())
     else:
         assert full is None
     dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,m,world", [(64, 64, 2), (64, 64, 3), (256, 256, 8), (7, 6, 2), (56, 56, 4)])
+def test_shard_ids_are_whole_trees(n, m, world):
+    """Shards partition the representatives into whole warm-start trees
+    (every parent in the same shard), balanced within one tree's size."""
+    level, parent, root = engine.warm_forest(n, m)
+    total = engine.half_grid_count(n, m)
+    shards = [shard_ids(n, m, g, world) for g in range(world)]
+    allids = np.concatenate(shards)
+    assert np.array_equal(np.sort(allids), np.arange(total))
+    biggest = np.bincount(root).max()
+    for ids in shards:
+        assert np.all(np.diff(ids) > 0)
+        par = parent[ids]
+        assert np.isin(par[par >= 0], ids).all()
+        assert abs(len(ids) - total / world) <= biggest
+    # plans restricted to a shard are the global plan's stages (sizes from the whole grid)
+    for ids in shards:
+        stages = engine.subset_plan(n, m, ids, "cpu")
+        got = sum(len(s[0]) for s in stages)
+        assert got == len(ids)
+        for sel, pred, gsize in stages:
+            assert gsize == np.count_nonzero(level == level[ids[sel.numpy()[0]]])
 
 
 @pytest.mark.parametrize("world,total", [(2, 11), (3, 10)])
