@@ -210,11 +210,11 @@ class TripletList:
             raise IndexError(f"frequency index {f} out of range for {self._n} frequencies")
         u, cj = int(self._rep[f]), bool(self._conj[f])
         Uf, Vf, sf = self._U[u], self._V[u], self._sig[u]
-        if cj:
-            Uf, Vf = Uf.conj(), Vf.conj()
+        if cj:  # materialised copies: a lazy torch conj view would reach the C-ABI unconjugated
+            Uf, Vf = Uf.conj().resolve_conj(), Vf.conj().resolve_conj()
         if self._host:
-            Uf = Uf.resolve_conj().cpu().numpy().astype(np.complex128)
-            Vf = Vf.resolve_conj().cpu().numpy().astype(np.complex128)
+            Uf = Uf.cpu().numpy().astype(np.complex128)
+            Vf = Vf.cpu().numpy().astype(np.complex128)
             sf = sf.cpu().numpy().astype(np.float64)
         k = (self._freqs[f, 0], self._freqs[f, 1])
         return SvdTriplet(k=k, U=Uf, sigma=sf, V=Vf)

@@ -110,7 +110,14 @@ def stream_ptr(device) -> int:
 
 
 def ptr(t) -> int:
-    return 0 if t is None else t.data_ptr()
+    """Raw device address for the C-ABI.  A lazily conjugated / negated torch
+    view shares the unconjugated storage, so handing its address to a kernel
+    would silently drop the conjugation: refuse it."""
+    if t is None:
+        return 0
+    if t.is_conj() or t.is_neg():
+        raise ValueError("lazily conjugated tensor passed to the C-ABI (call resolve_conj() first)")
+    return t.data_ptr()
 
 
 class _Workspace:
@@ -646,7 +653,7 @@ class Timer:
 def materialize_vector(factor, col: int, fi: int, fj: int, n: int, m: int, dtype: str):
     rows, r = factor.shape
     out = torch.empty((n * m * rows,), dtype=complex_dtype(dtype), device=factor.device)
-    st = _lib.load().cs_materialize_vector(ptr(factor.contiguous()), dtype_code(dtype), rows, r,
+    st = _lib.load().cs_materialize_vector(ptr(factor.resolve_conj().contiguous()), dtype_code(dtype), rows, r,
                                            col, fi, fj, n, m, ptr(out),
                                            stream_ptr(factor.device))
     _lib.check(st, "cs_materialize_vector")
