@@ -256,7 +256,8 @@ static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
 
 // tensor-core blocked kernel (cs_tcb.cu): fp32, vectors, instantiated shapes
 bool tcb_supported(int mr, int nc, bool wantv);
-int tcb_dispatch(const JacArgs<float> &a, cudaStream_t st);
+size_t tcb_workspace(int mr, int nc, bool wantv);
+int tcb_dispatch(const JacArgs<float> &a, void *ws, size_t ws_bytes, cudaStream_t st);
 // experiment switch, read once: CS_TCB=0 keeps the scalar panel kernel
 static bool tcb_enabled() {
     static const bool on = [] {
@@ -278,6 +279,10 @@ static int svd_workspace(long long count, int co, int ci, bool wantv, size_t *by
     *bytes = 0;
     if (count <= 0) return CS_OK;
     if (!plan<T>(co, ci, wantv, count, s)) return fail(CS_EINVAL, "batched SVD: no plan");
+    // warm-started solves of tcb shapes run the tensor-core kernel, whose
+    // groups exchange panels through mailboxes in the workspace
+    const size_t tcb_bytes = (sizeof(T) == 4 && tcb_enabled()) ? tcb_workspace(s.mr, s.nc, wantv) : 0;
+    *bytes = tcb_bytes;
     if (s.smem_resident) return CS_OK;
     JacArgs<T> a = {};
     a.count = count;
@@ -285,7 +290,7 @@ static int svd_workspace(long long count, int co, int ci, bool wantv, size_t *by
     long long ncl = 0;
     int st = dispatch<T>(a, wantv, 0, true, &ncl);
     if (st) return st;
-    *bytes = (size_t)ncl * s.C * s.scratch_per_cta * 2 * sizeof(T);
+    *bytes = std::max(tcb_bytes, (size_t)ncl * s.C * s.scratch_per_cta * 2 * sizeof(T));
     return CS_OK;
 }
 
@@ -330,7 +335,8 @@ static int svd_run(const void *blocks, long long count, int co, int ci, bool wan
     if constexpr (sizeof(T) == 4) {
         // warm-started solves only: cold starts (large rotations in every early
         // sweep) are faster on the scalar panel kernel
-        if (tcb_enabled() && a.initX && tcb_supported(a.s.mr, a.s.nc, wantv)) return tcb_dispatch(a, st);
+        if (tcb_enabled() && a.initX && tcb_supported(a.s.mr, a.s.nc, wantv))
+            return tcb_dispatch(a, ws, ws_bytes, st);
     }
     return dispatch<T>(a, wantv, st, false, nullptr);
 }

@@ -1,11 +1,10 @@
 // cs_tcb.cu -- K3 "tcb": tensor-core blocked one-sided Jacobi for large
 // blocks with vectors (fp32; cfg5's 256 x 256 + V).
 //
-// Same partition and block-circle ordering as the panel kernel
-// (cs_panel.cuh): a cluster of C CTAs holds one matrix, CTA c owns two
-// panels of W = 16 columns (all X and V rows), and 2C-1 super-rounds per
-// sweep pair every panel with every other.  What changes is how a
-// super-round treats its panel pair P = [a b] (X rows then V rows):
+// A group of C CTAs solves one matrix; CTA c holds two panels of W = 16
+// columns (all X and V rows), and 2C-1 super-rounds per sweep pair every
+// panel with every other.  A super-round treats its panel pair P = [a b]
+// (X rows then V rows):
 //
 //   1. G = P_X^H P_X on tcgen05 (3xTF32, 64 x 64 real, 4 row stages whose
 //      TMEM accumulators are summed in fp32);
@@ -21,24 +20,42 @@
 // column pair is tested once per sweep; a sweep in which no pair passes
 // the threshold ends the solve exactly as in the reference (blocksvd.py:
 // 121-123).  Simultaneous rotations replace the w sequential rounds whose
-// dependency chain bounds the scalar kernel; a CPU study of the block
-// ordering (warm-started cfg5 blocks, f64) needs 6.8 instead of 6.0 sweeps.
+// dependency chain bounds the scalar kernel.
 //
-// The panels live in shared memory in the 128-byte-swizzled K-major layout
-// the update reads directly (cs_tcb.cuh); the Gram reads a transposed hi|lo
-// copy staged per 64 rows.  Between super-rounds panels move across the
-// cluster through DSMEM as in the panel kernel.
+// Panel exchange (the part that bounds a super-round once the O(rows) work
+// is on the tensor cores).  The 2C-1 pairings of a sweep are a fixed
+// 1-factorisation of the 2C panels (circle method on panel labels); between
+// two consecutive pairings every CTA keeps one panel and swaps the other --
+// possible for ANY two perfect matchings (their union is a set of even
+// alternating cycles; orienting each cycle gives every CTA one panel in and
+// one out).  So only ONE panel (64 KB) moves per CTA and super-round instead
+// of two, and odd sweeps run the pairings backwards (no exchange at sweep
+// boundaries).  Panels move through L2 rather than DSMEM: the sender pushes
+// the outgoing panel into its mailbox in global memory with TMA bulk stores
+// (X rows first, then V rows, each published by a release flag); the
+// receiver pulls it with TMA bulk loads into its free shared-memory slot and
+// acknowledges.  No cluster barrier, only pairwise flags: a CTA waits only
+// for the one CTA it receives from.  Without the cluster-placement limit
+// (15 clusters of 8 = 120 SMs) the groups fill 144 of 148 SMs; co-residency
+// of a group's CTAs is guaranteed by a cooperative launch.
+//
+// Shared memory: three 64 KB slots (panel a, panel b, scratch) whose roles
+// rotate -- the incoming panel lands in the scratch slot, the outgoing
+// panel's slot becomes the next scratch.
+#include <cstdio>
+
 #include "cs_tcb.cuh"
 
 namespace cs {
 namespace tcb {
 
 constexpr int NT = 512;
+constexpr int MAXC = 8;
 
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
-__device__ unsigned long long g_tcb_cycles[10];  // [7] cluster wait, [9] super-round count
+__device__ unsigned long long g_tcb_cycles[16];  // [9] super-round count, [10..15] exchange sub-steps
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
         if (tid == 0) {                                                              \
@@ -47,37 +64,109 @@ __device__ unsigned long long g_tcb_cycles[10];  // [7] cluster wait, [9] super-
             tcb_t = _c;                                                              \
         }                                                                            \
     } while (0)
+#define TCB_SUB(i)                                                                   \
+    do {                                                                             \
+        const long long _c = clock64();                                              \
+        atomicAdd(&g_tcb_cycles[i], (unsigned long long)(_c - tcb_s));               \
+        tcb_s = _c;                                                                  \
+    } while (0)
 #else
 #define TCB_MARK(i) do { } while (0)
+#define TCB_SUB(i) do { } while (0)
 #endif
+
+// the sweep's pairings and the exchange between consecutive ones (host-built)
+struct Sched {
+    signed char ida[2 * MAXC - 1][MAXC], idb[2 * MAXC - 1][MAXC];  // panels of CTA c at step t
+    signed char src[2 * MAXC - 2][MAXC], dst[2 * MAXC - 2][MAXC];  // exchange t -> t+1
+};
+
+// global-memory coordination area of a launch (inside the SVD workspace)
+struct Ws {
+    unsigned char *ctrl;  // per CTA 256 B: flags (see CT_*)
+    float *gsig;          // per group [2][NC] squared column norms (epilogue)
+    unsigned char *mail;  // per CTA [2] outgoing panels
+    int ngroups;
+};
+constexpr int CT_FX = 0, CT_FV = 32, CT_ACK = 64, CT_VERD = 96, CT_EPI = 160, CT_BYTES = 256;  // ACK/VERD/EPI: [2] by parity
 
 template <int MR, int NC>
 struct Cfg {
     static constexpr int C = NC / N2;
+    static constexpr int STEPS = 2 * C - 1;
     static constexpr int ROWS = MR + NC;
-    static constexpr uint32_t ATOM = ROWS * 128;
-    static constexpr uint32_t RG_OFF = 2 * ATOM;
-    static constexpr uint32_t RG_BYTES = 65536;
-    static constexpr uint32_t SIG_OFF = RG_OFF + RG_BYTES;
+    static constexpr uint32_t SLOT = ROWS * 128;  // one panel: W complex = 32 real columns, SW128 K-major
+    static constexpr uint32_t XBYTES = MR * 128;  // its X rows (the V rows follow)
+    static constexpr uint32_t SIG_OFF = 3 * SLOT;
     static constexpr uint32_t PERM_OFF = SIG_OFF + NC * 4;
     static constexpr uint32_t FLAG_OFF = PERM_OFF + 2 * NC * 4;
-    static constexpr uint32_t RED_OFF = FLAG_OFF + 68 * 4;
+    static constexpr uint32_t RED_OFF = FLAG_OFF + 16 * 4;
     static constexpr uint32_t BAR_OFF = (RED_OFF + 64 * 4 + 15) & ~15u;
     static constexpr uint32_t TM_OFF = BAR_OFF + 4 * 8;
     static constexpr uint32_t SMEM = TM_OFF + 16;
     static constexpr int STAGES = MR / 64;
     static constexpr int MBLK = ROWS / 128;
     static_assert(MR % 64 == 0 && ROWS % 128 == 0 && NC % N2 == 0, "tcb shape");
+    static_assert(SLOT >= 65536, "tcb scratch slot holds the 64 KB Gram/update staging");
     static_assert(STAGES <= 4 && MBLK <= 4, "tcb TMEM budget (4 accumulators of 128 columns)");
-    static_assert(C >= 2 && C <= 8, "tcb cluster size");
+    static_assert(C >= 2 && C <= MAXC, "tcb group size");
     static_assert(SMEM <= 227 * 1024, "tcb shared memory");
 };
 
-// scratch offsets inside the region during the rotation phase (bytes)
+// byte offset of (row r, real column k < 32) inside one panel slot, and of
+// the 16-byte chunk k4 < 8 of row r (the pair layout of cs_tcb.cuh, one atom)
+__device__ __forceinline__ uint32_t so(int r, int k) { return sw_off(r, k, 0); }
+__device__ __forceinline__ uint32_t so4(int r, int k4) { return sw_chunk(r, k4, 0); }
+
+// scratch offsets inside the scratch slot during the rotation phase (bytes)
 // (HH, HL: real 64 x 65 partial Grams read from TMEM; dead once G is built)
 constexpr uint32_t SC_D = 0, SC_PRM = 8448, SC_E = 16384, SC_T = 24832, SC_HH = 0, SC_HL = 16640, SC_G = 33792,
                    SC_BOP = 32768;
 constexpr int LDR = 65;
+
+// ---- global-memory flags and TMA bulk copies ------------------------------
+__device__ __forceinline__ unsigned ld_acq(const void *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel(void *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_but1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
+
+// a group peer that never arrives (it cannot: the launch is cooperative)
+// must not hang the GPU: trap after ~10 s of polling
+__device__ __noinline__ void spin_timeout(int what) {
+    printf("jacobi_tcb_kernel: block %d timed out waiting on a group peer (%d)\n", (int)blockIdx.x, what);
+    __trap();
+}
+__device__ __forceinline__ void spin_ge(const void *p, unsigned v, int what) {
+    unsigned n = 0;
+    while ((int)(ld_acq(p) - v) < 0) {
+        if (++n > (1u << 25)) spin_timeout(what);
+        __nanosleep(32);
+    }
+}
+__device__ __forceinline__ unsigned spin_tag(const void *p, unsigned tag, int what) {
+    unsigned n = 0, v;
+    while (((v = ld_acq(p)) >> 2) != tag) {
+        if (++n > (1u << 25)) spin_timeout(what);
+        __nanosleep(32);
+    }
+    return v;
+}
 
 // C = s * A B (+ I) on 32 x 32 complex matrices in shared memory (stride LDG)
 __device__ __forceinline__ void cgemm32(const float2 *A, const float2 *B, float2 *Cm, float s, bool addI) {
@@ -156,29 +245,50 @@ __device__ void expm_minus_identity(float2 *Em, float2 *Tm, float2 *Dm, float *r
     }
 }
 
+// Gram stage: rows [r0, r0+64) of the X rows of the pair (a: real columns
+// 0..31, b: 32..63) -> the transposed hi|lo staging (cs_tcb.cuh gram_stage)
+__device__ __forceinline__ void gram_stage2(const unsigned char *Pa, const unsigned char *Pb, int r0,
+                                            unsigned char *stg) {
+#pragma unroll
+    for (int i = 0; i < 1024 / NT; ++i) {
+        const int u = threadIdx.x + i * NT, j = u & 63, rq = u >> 6;
+        const unsigned char *P = j < 32 ? Pa : Pb;
+        const int k = j & 31;
+        float4 h;
+        h.x = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 0, k));
+        h.y = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 1, k));
+        h.z = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 2, k));
+        h.w = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 3, k));
+        // round-to-nearest split (hi symmetric around x): the dropped lo*lo
+        // term is then unbiased
+        const float4 hr = make_float4(rna_tf32(h.x), rna_tf32(h.y), rna_tf32(h.z), rna_tf32(h.w));
+        const float4 lr = make_float4(rna_tf32(h.x - hr.x), rna_tf32(h.y - hr.y), rna_tf32(h.z - hr.z),
+                                      rna_tf32(h.w - hr.w));
+        *reinterpret_cast<float4 *>(stg + sw_chunk(j, rq, 16384)) = hr;
+        *reinterpret_cast<float4 *>(stg + sw_chunk(64 + j, rq, 16384)) = lr;
+    }
+}
+
 template <int MR, int NC>
-__global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> a) {
+__global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> a, const Sched sc, const Ws ws) {
     using K = Cfg<MR, NC>;
-    constexpr int C = K::C;
-    constexpr uint32_t ATOM = K::ATOM;
+    constexpr int C = K::C, STEPS = K::STEPS;
+    constexpr uint32_t SLOT = K::SLOT, XBYTES = K::XBYTES;
     extern __shared__ __align__(1024) unsigned char sm[];
-    unsigned char *AB = sm;
-    unsigned char *RG = sm + K::RG_OFF;
     float *sig2 = reinterpret_cast<float *>(sm + K::SIG_OFF);
     int *perm = reinterpret_cast<int *>(sm + K::PERM_OFF);
     int *flags = reinterpret_cast<int *>(sm + K::FLAG_OFF);
-    int *pos = flags + 4;
     float *red = reinterpret_cast<float *>(sm + K::RED_OFF);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);  // [0,1] MMA ring, [2] X in, [3] V in
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + K::TM_OFF);
-    float2 *Dm = reinterpret_cast<float2 *>(RG + SC_D);
-    float2 *Gm = reinterpret_cast<float2 *>(RG + SC_G);
-    unsigned char *Bop = RG + SC_BOP;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rank = (int)cg::this_cluster().block_rank();
-    const long long cid = blockIdx.x / C;
+    const int g = blockIdx.x / C, rank = blockIdx.x % C;
     const float tol = a.tol;
+    unsigned char *const myctl = ws.ctrl + (size_t)blockIdx.x * CT_BYTES;
+    auto ctl = [&](int cta) { return ws.ctrl + ((size_t)g * C + cta) * CT_BYTES; };
+    auto box = [&](int cta, int par) { return ws.mail + (((size_t)g * C + cta) * 2 + par) * SLOT; };
+    float *const gsig = ws.gsig + (size_t)g * 2 * NC;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -192,22 +302,26 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    uint32_t ph1 = 0, ph2 = 0;  // parities of the two ring barriers (bar[1], bar[2])
+    uint32_t ph1 = 0, ph2 = 0, phx = 0, phv = 0;  // mbarrier parities (uniform over the CTA)
     auto ring_wait = [&](int slot) {
-        if (slot == 0) { mbar_wait(&bar[1], ph1); ph1 ^= 1; }
-        else { mbar_wait(&bar[2], ph2); ph2 ^= 1; }
+        if (slot == 0) { mbar_wait(&bar[0], ph1); ph1 ^= 1; }
+        else { mbar_wait(&bar[1], ph2); ph2 ^= 1; }
     };
+    unsigned epoch = 0, vseq = 0, mseq = 0;  // exchanges, sweeps, matrices of this launch (group-uniform)
 
-    for (long long f = cid; f < a.count; f += a.s.num_clusters) {
+    for (long long f = g; f < a.count; f += ws.ngroups) {
         const long long mid = a.index ? a.index[f] : f;
-        if (tid < 2 * C) pos[tid] = tid;
-        // ---- load the two panels: a = columns [rank W, +W), b = [(2C-1-rank) W, +W)
+        ++mseq;
+        int sl[3] = {0, 1, 2};  // slots of panel a, panel b, scratch
+        int ia = sc.ida[0][rank], ib = sc.idb[0][rank];
+        // ---- load the two panels (panel x = working columns [x W, x W + W))
         {
             const float2 *X0 = a.initX ? a.initX + (size_t)f * MR * NC : nullptr;
             const float2 *V0 = a.initV ? a.initV + (size_t)a.initV_index[f] * NC * NC : nullptr;
             const float2 *A = a.blocks + (size_t)mid * a.co * a.ci;
             for (int half = 0; half < 2; ++half) {
-                const int c0 = (half == 0 ? rank : 2 * C - 1 - rank) * W;
+                const int c0 = (half == 0 ? ia : ib) * W;
+                unsigned char *P = sm + sl[half] * SLOT;
                 for (int idx = tid; idx < K::ROWS * W; idx += NT) {
                     const int r = idx / W, jj = idx % W, j = c0 + jj;
                     float2 v;
@@ -220,35 +334,59 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         if (V0) v = V0[(size_t)rv * NC + j];
                         else v = make_float2(rv == j ? 1.f : 0.f, 0.f);
                     }
-                    *reinterpret_cast<float2 *>(AB + sw_off(r, 32 * half + 2 * jj, ATOM)) = v;
+                    *reinterpret_cast<float2 *>(P + so(r, 2 * jj)) = v;
                 }
             }
         }
         __syncthreads();
 
         int info = -1;
+        bool wait_x = false, wait_v = false;  // incoming panel (in flight into slot a or b)
+        int src_pending = 0;
+        auto finish_v = [&]() {  // the incoming V rows have landed: acknowledge the sender's mailbox
+            if (wait_v) {
+                mbar_wait(&bar[3], phv);
+                phv ^= 1;
+                wait_v = false;
+                if (tid == 0) st_rel(ctl(src_pending) + CT_ACK + 4 * (epoch & 1), epoch);
+            }
+        };
         for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+            const bool fwd = (sweep & 1) == 0;
             bool rot = false, bad = false;
 #pragma unroll 1
-            for (int t = 0; t < 2 * C - 1; ++t) {
-                const bool full = (t == 0);
+            for (int i = 0; i < STEPS; ++i) {
+                const int t = fwd ? i : STEPS - 1 - i;
+                const bool full = (i == 0);
 #ifdef CS_TCB_CLOCKS
                 long long tcb_t = clock64();
                 if (tid == 0) atomicAdd(&g_tcb_cycles[9], 1ull);
 #endif
+                unsigned char *const Pa = sm + sl[0] * SLOT;
+                unsigned char *const Pb = sm + sl[1] * SLOT;
+                unsigned char *const RG = sm + sl[2] * SLOT;
+                float2 *Dm = reinterpret_cast<float2 *>(RG + SC_D);
+                float2 *Gm = reinterpret_cast<float2 *>(RG + SC_G);
+                unsigned char *Bop = RG + SC_BOP;
+                if (wait_x) {
+                    mbar_wait(&bar[2], phx);
+                    phx ^= 1;
+                    wait_x = false;
+                }
+                TCB_MARK(7);
                 // ---- (1) Gram: STAGES x 64 X rows, transposed hi|lo staging, 2-slot ring
 #pragma unroll 1
                 for (int st = 0; st < K::STAGES; ++st) {
                     const int slot = st & 1;
                     if (st >= 2) ring_wait(slot);
-                    gram_stage<NT>(AB, ATOM, 64 * st, RG + slot * 32768);
+                    gram_stage2(Pa, Pb, 64 * st, RG + slot * 32768);
                     fence_proxy_async_smem();
                     __syncthreads();
                     if (warp == (st & 3)) {  // one issuing warp per stage (issuers overlap)
                         if (lane == 0) {
                             tc_after_sync();
                             gram_mma(tmem + 128 * (st & 3), smem_u32(RG + slot * 32768));
-                            mma_commit(&bar[1 + slot]);
+                            mma_commit(&bar[slot]);
                         }
                         __syncwarp();
                     }
@@ -268,27 +406,27 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     if (q < 2) {  // lanes 0..63: warps with quarter 0, 1; 32 columns each
                         float acc[32];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+                        for (int i2 = 0; i2 < 32; ++i2) acc[i2] = 0.f;
 #pragma unroll 1
                         for (int st = 0; st < K::STAGES; ++st) {
                             float v[16];
                             tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * st + cb, v);
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) acc[i] += v[i];
+                            for (int i2 = 0; i2 < 16; ++i2) acc[i2] += v[i2];
                             tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * st + cb + 16, v);
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) acc[16 + i] += v[i];
+                            for (int i2 = 0; i2 < 16; ++i2) acc[16 + i2] += v[i2];
                         }
                         const int row = 32 * q + lane;
-                        float *dst = cb < 64 ? HH + row * LDR + cb : HL + row * LDR + (cb - 64);
+                        float *dstp = cb < 64 ? HH + row * LDR + cb : HL + row * LDR + (cb - 64);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) dst[i] = acc[i];
+                        for (int i2 = 0; i2 < 32; ++i2) dstp[i2] = acc[i2];
                     }
                     tc_before_sync();
                     __syncthreads();
                     for (int x = tid; x < N2 * N2; x += NT) {
                         const int c = x >> 5, j = x & 31;
-                        auto R = [&](int i, int k) { return HH[i * LDR + k] + HL[i * LDR + k] + HL[k * LDR + i]; };
+                        auto R = [&](int i2, int k) { return HH[i2 * LDR + k] + HL[i2 * LDR + k] + HL[k * LDR + i2]; };
                         // G_r = R[2c][2j] + R[2c+1][2j+1], G_i = R[2c][2j+1] - R[2c+1][2j]
                         Gm[c * LDG + j] = make_float2(R(2 * c, 2 * j) + R(2 * c + 1, 2 * j + 1),
                                                       R(2 * c, 2 * j + 1) - R(2 * c + 1, 2 * j));
@@ -306,9 +444,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 if (tid < nround * W) {
                     int p, qq;
                     inner_pair(full, tid % W, tid / W, p, qq);
-                    const float2 g = Gm[p * LDG + qq];
+                    const float2 gv = Gm[p * LDG + qq];
                     Rot<float> R;
-                    act = rot_params<float>(Gm[p * LDG + p].x, Gm[qq * LDG + qq].x, g.x, g.y, tol, R);
+                    act = rot_params<float>(Gm[p * LDG + p].x, Gm[qq * LDG + qq].x, gv.x, gv.y, tol, R);
                     Prm<float> pm;
                     pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
                     prm[tid] = pm;
@@ -324,21 +462,21 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         // GCHECK_TAU): D = Q - I for Q = the product of the rounds'
                         // rotations, D <- D J_r + (J_r - I).  Rows evolve independently,
                         // so the 16 threads of a row (half a warp) only sync warp-wide.
-                        const int i = tid >> 4, k = tid & 15;
+                        const int i2 = tid >> 4, k = tid & 15;
 #pragma unroll 1
                         for (int r = 0; r < nround; ++r) {
                             const Prm<float> pm = prm[r * W + k];
                             if (pm.act > 0) {
                                 int p, qq;
                                 inner_pair(full, k, r, p, qq);
-                                float2 x = Dm[i * LDG + p], y = Dm[i * LDG + qq];
+                                float2 x = Dm[i2 * LDG + p], y = Dm[i2 * LDG + qq];
                                 Rot<float> R;
                                 R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
                                 rot_apply<float>(x, y, R);
-                                if (i == p) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
-                                if (i == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
-                                Dm[i * LDG + p] = x;
-                                Dm[i * LDG + qq] = y;
+                                if (i2 == p) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
+                                if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
+                                Dm[i2 * LDG + p] = x;
+                                Dm[i2 * LDG + qq] = y;
                             }
                             __syncwarp();
                         }
@@ -359,9 +497,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                                 inner_pair(full, tid % W, tid / W, p, qq);
                                 const float sn = sqrtf(pm.wr * pm.wr + pm.wi * pm.wi);  // sin(theta)
                                 const float th = atan2f(sn, 1.f + pm.cm1);
-                                const float f = th / sn;
-                                Em[p * LDG + qq] = make_float2(f * pm.wr, f * pm.wi);
-                                Em[qq * LDG + p] = make_float2(-f * pm.wr, f * pm.wi);
+                                const float fc = th / sn;
+                                Em[p * LDG + qq] = make_float2(fc * pm.wr, fc * pm.wi);
+                                Em[qq * LDG + p] = make_float2(-fc * pm.wr, fc * pm.wi);
                             }
                         }
                         __syncthreads();
@@ -370,16 +508,17 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     TCB_MARK(3);
                     // ---- (5) B operand (D~, hi | lo) and (6) update P += P D
                     build_bop<NT>(Dm, Bop);
+                    finish_v();       // the V rows of an incoming panel are needed from here
                     __syncthreads();  // D read before the ring (aliasing it) is written
 #pragma unroll 1
                     for (int ch = 0; ch < 2 * K::MBLK; ++ch) {
                         const int mb = ch >> 1, at = ch & 1, slot = ch & 1;
                         if (ch >= 2) ring_wait(slot);
                         unsigned char *lo = RG + slot * 16384;
-                        const unsigned char *srcp = AB + at * ATOM + mb * 16384;
+                        const unsigned char *srcp = (at ? Pb : Pa) + mb * 16384;
 #pragma unroll
-                        for (int i = 0; i < 1024 / NT; ++i) {
-                            const int u = tid + i * NT;
+                        for (int i2 = 0; i2 < 1024 / NT; ++i2) {
+                            const int u = tid + i2 * NT;
                             *reinterpret_cast<float4 *>(lo + 16 * u) =
                                 lo4(*reinterpret_cast<const float4 *>(srcp + 16 * u));
                         }
@@ -399,7 +538,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                                     mma_tf32(d, dah, db, IDESC_UPD, acc0);          // [hi*hi | hi*lo]
                                     mma_tf32(d + 64, dal, db, IDESC_UPD_LO, 1u);    // + lo*hi -> correction
                                 }
-                                mma_commit(&bar[1 + slot]);
+                                mma_commit(&bar[slot]);
                             }
                             __syncwarp();
                         }
@@ -408,7 +547,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     ring_wait(1);
                     tc_after_sync();
                     TCB_MARK(4);
-                    // ---- (7) P += acc: warp group g -> M-blocks g, g+4, ..; quarter q -> lanes
+                    // ---- (7) P += acc: warp group -> M-blocks, quarter q -> lanes;
+                    // output real column n -> chunk n/4 of panel a (n < 32) or b
                     {
                         const int q = warp & 3;
 #pragma unroll 1
@@ -420,10 +560,11 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                                 tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 16 * c, v);
                                 tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 64 + 16 * c, vc);
 #pragma unroll
-                                for (int i = 0; i < 16; ++i) v[i] += vc[i];
+                                for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
-                                    float4 *pp = reinterpret_cast<float4 *>(AB + sw_chunk(row, 4 * c + u, ATOM));
+                                    const int k4 = 4 * c + u;
+                                    float4 *pp = reinterpret_cast<float4 *>((k4 < 8 ? Pa : Pb) + so4(row, k4 & 7));
                                     float4 x = *pp;
                                     x.x += v[4 * u]; x.y += v[4 * u + 1]; x.z += v[4 * u + 2]; x.w += v[4 * u + 3];
                                     *pp = x;
@@ -433,62 +574,76 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         tc_before_sync();
                     }
                 }
+                finish_v();
+                fence_proxy_async_smem();  // panel writes -> the TMA store of the outgoing panel
                 __syncthreads();
                 TCB_MARK(5);
-                // ---- (8) panel rotation across the cluster (circle method over 2C
-                // positions, position 0 fixed): new a <- position rank+1, new b <-
-                // position 2C-rank; staged through registers (peers read this CTA's
-                // panels until the second cluster barrier)
-                if (t < 2 * C - 2) {
-                    cluster_sync_all();
-                    TCB_MARK(7);  // waiting for the slowest CTA of the cluster
-                    const uint32_t own = smem_u32(AB);
-                    const uint32_t src_a = rank == 0 ? own : (rank == C - 1 ? own + ATOM : map_rank(own, rank + 1));
-                    const uint32_t src_b = rank == 0 ? map_rank(own, 1) : map_rank(own + ATOM, rank - 1);
-                    constexpr int PER = (int)(ATOM / 16 / NT);
-                    float4 ra[PER], rb[PER];
-#pragma unroll
-                    for (int i = 0; i < PER; ++i) {
-                        const uint32_t o = 16u * (tid + i * NT);
-                        if (rank != 0) {
-                            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                         : "=f"(ra[i].x), "=f"(ra[i].y), "=f"(ra[i].z), "=f"(ra[i].w)
-                                         : "r"(src_a + o) : "memory");
-                        }
-                        asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                     : "=f"(rb[i].x), "=f"(rb[i].y), "=f"(rb[i].z), "=f"(rb[i].w)
-                                     : "r"(src_b + o) : "memory");
+                // ---- (8) exchange to the next pairing: keep one panel, send the other
+                // to dst's mailbox, receive the new one from src's into the scratch slot
+                if (i < STEPS - 1) {
+                    const int t2 = fwd ? t + 1 : t - 1;
+                    const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;  // outgoing role
+                    const int src = fwd ? sc.src[t][rank] : sc.dst[t2][rank];
+                    ++epoch;
+                    const int par = epoch & 1;
+                    if (tid == 0) {
+#ifdef CS_TCB_CLOCKS
+                        long long tcb_s = clock64();
+#endif
+                        if (epoch > 2) spin_ge(myctl + CT_ACK + 4 * par, epoch - 2, 1);  // mailbox consumed
+                        TCB_SUB(10);
+                        unsigned char *mb = box(rank, par);
+                        const uint32_t os = smem_u32(sm + sl[o] * SLOT);
+                        bulk_s2g(mb, os, XBYTES);
+                        bulk_commit();
+                        bulk_s2g(mb + XBYTES, os + XBYTES, SLOT - XBYTES);
+                        bulk_commit();
+                        bulk_wait_read_all();  // the outgoing slot is free (next scratch)
+                        TCB_SUB(11);
+                        bulk_wait_but1();
+                        fence_proxy_async_global();
+                        st_rel(myctl + CT_FX, epoch);
+                        TCB_SUB(12);
+                        bulk_wait_all();
+                        fence_proxy_async_global();
+                        st_rel(myctl + CT_FV, epoch);
+                        TCB_SUB(13);
+                        const unsigned char *in = box(src, par);
+                        const uint32_t is = smem_u32(sm + sl[2] * SLOT);
+                        spin_ge(ctl(src) + CT_FX, epoch, 2);
+                        fence_proxy_async_global();
+                        mbar_arrive_expect_tx(&bar[2], XBYTES);
+                        bulk_g2s(is, in, XBYTES, smem_u32(&bar[2]));
+                        TCB_SUB(14);
+                        spin_ge(ctl(src) + CT_FV, epoch, 3);
+                        fence_proxy_async_global();
+                        mbar_arrive_expect_tx(&bar[3], SLOT - XBYTES);
+                        bulk_g2s(is + XBYTES, in + XBYTES, SLOT - XBYTES, smem_u32(&bar[3]));
+                        TCB_SUB(15);
                     }
-                    int np = 0;
-                    if (tid < 2 * C) np = (tid == 0) ? pos[0] : (tid == 2 * C - 1 ? pos[1] : pos[tid + 1]);
-                    cluster_sync_all();
-#pragma unroll
-                    for (int i = 0; i < PER; ++i) {
-                        const uint32_t o = 16u * (tid + i * NT);
-                        if (rank != 0) *reinterpret_cast<float4 *>(AB + o) = ra[i];
-                        *reinterpret_cast<float4 *>(AB + ATOM + o) = rb[i];
-                    }
-                    if (tid < 2 * C) pos[tid] = np;
+                    wait_x = wait_v = true;
+                    src_pending = src;
+                    const int ns = sl[2];
+                    sl[2] = sl[o];
+                    sl[o] = ns;
+                    ia = sc.ida[t2][rank];
+                    ib = sc.idb[t2][rank];
                     __syncthreads();
                 }
                 TCB_MARK(6);
             }
-            // ---- sweep verdict, OR-ed over the cluster
+            // ---- sweep verdict, OR-ed over the group (double-buffered by sweep parity)
+            ++vseq;
             if (tid == 0) {
-                flags[0] = rot ? 1 : 0;
-                flags[1] = bad ? 1 : 0;
+                st_rel(myctl + CT_VERD + 4 * (vseq & 1), (vseq << 2) | (bad ? 2u : 0u) | (rot ? 1u : 0u));
+                unsigned any = 0;
+                for (int d = 0; d < C; ++d) any |= spin_tag(ctl(d) + CT_VERD + 4 * (vseq & 1), vseq, 4);
+                flags[0] = any & 1;
+                flags[1] = (any >> 1) & 1;
             }
-            cluster_sync_all();
-            int any_rot = 0, any_bad = 0;
-            {
-                cg::cluster_group cl = cg::this_cluster();
-                for (int d = 0; d < C; ++d) {
-                    const int *pf = cl.map_shared_rank(flags, d);
-                    any_rot |= pf[0];
-                    any_bad |= pf[1];
-                }
-            }
-            cluster_sync_all();
+            __syncthreads();
+            const int any_rot = flags[0], any_bad = flags[1];
+            __syncthreads();
             if (any_bad) break;
             if (!any_rot) {
                 info = sweep + 1;
@@ -497,35 +652,29 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         }
 
         // ---- epilogue: exact fp32 column norms of the local panels, gathered
-        // over the cluster; stable descending order; U = X / sigma, V
-        const int pa = pos[rank], pb = pos[2 * C - 1 - rank];
+        // over the group through global memory; stable descending order;
+        // U = X / sigma, V
+        float *gs = gsig + (mseq & 1) * NC;
         for (int c = warp; c < N2; c += NT / 32) {
             const int half = c / W, jj = c % W;
+            const unsigned char *P = sm + sl[half] * SLOT;
             float acc = 0.f;
             for (int r = lane; r < MR; r += 32) {
-                const float2 v = *reinterpret_cast<const float2 *>(AB + sw_off(r, 32 * half + 2 * jj, ATOM));
+                const float2 v = *reinterpret_cast<const float2 *>(P + so(r, 2 * jj));
                 acc = fmaf(v.x, v.x, fmaf(v.y, v.y, acc));
             }
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) sig2[(half == 0 ? pa : pb) * W + jj] = acc;
+            if (lane == 0) gs[(half == 0 ? ia : ib) * W + jj] = acc;
         }
-        cluster_sync_all();
-        {
-            float *stage = reinterpret_cast<float *>(RG);
-            cg::cluster_group cl = cg::this_cluster();
-            for (int j = tid; j < NC; j += NT) {
-                const int panel = j / W;
-                int p0 = 0;
-                for (int p = 0; p < 2 * C; ++p)
-                    if (pos[p] == panel) p0 = p;
-                const int owner = pos_owner(p0, C);
-                stage[j] = owner == rank ? sig2[j] : cl.map_shared_rank(sig2, owner)[j];
-            }
-            cluster_sync_all();
-            for (int j = tid; j < NC; j += NT) sig2[j] = sqrtf(stage[j]);
-            __syncthreads();
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_rel(myctl + CT_EPI + 4 * (mseq & 1), mseq);
+            for (int d = 0; d < C; ++d) spin_ge(ctl(d) + CT_EPI + 4 * (mseq & 1), mseq, 5);
         }
+        __syncthreads();
+        for (int j = tid; j < NC; j += NT) sig2[j] = sqrtf(__ldcg(gs + j));
         for (int j = tid; j < NC; j += NT) perm[j] = j;
         __syncthreads();
         if (info >= 0) {
@@ -552,13 +701,14 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         for (int p = tid; p < NC; p += NT) ipos[perm[p]] = p;
         __syncthreads();
         for (int half = 0; half < 2; ++half) {
-            const int c0 = (half == 0 ? pa : pb) * W;
+            const int c0 = (half == 0 ? ia : ib) * W;
+            const unsigned char *P = sm + sl[half] * SLOT;
             if (a.Uw) {
                 for (int idx = tid; idx < MR * W; idx += NT) {
                     const int r = idx / W, jj = idx % W, j = c0 + jj;
                     const float sj = sig2[j];
                     const float den = sj > 0.f ? sj : 1.f;
-                    const float2 v = *reinterpret_cast<const float2 *>(AB + sw_off(r, 32 * half + 2 * jj, ATOM));
+                    const float2 v = *reinterpret_cast<const float2 *>(P + so(r, 2 * jj));
                     a.Uw[((size_t)mid * MR + r) * NC + ipos[j]] = make_float2(__fdividef(v.x, den), __fdividef(v.y, den));
                 }
             }
@@ -566,7 +716,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 for (int idx = tid; idx < NC * W; idx += NT) {
                     const int r = idx / W, jj = idx % W, j = c0 + jj;
                     a.Vw[((size_t)mid * NC + r) * NC + ipos[j]] =
-                        *reinterpret_cast<const float2 *>(AB + sw_off(MR + r, 32 * half + 2 * jj, ATOM));
+                        *reinterpret_cast<const float2 *>(P + so(MR + r, 2 * jj));
                 }
             }
         }
@@ -575,7 +725,6 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
             for (int j = 0; j < NC; ++j) z |= !(sig2[j] > 0.f);
             a.zero_sigma[mid] = z;
         }
-        cluster_sync_all();  // peers done reading this CTA's buffers
         __syncthreads();
     }
     tc_before_sync();
@@ -583,33 +732,140 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// circle-method round r, slot k -> panels (p, q) (cs_jacobi.cuh pair_cols)
+static void pair_host(int k, int r, int np, int &p, int &q) {
+    const int L = np - 1;
+    int ca = 0;
+    if (k != 0) {
+        ca = k - 1 + r;
+        if (ca >= L) ca -= L;
+        ca += 1;
+    }
+    int cb = np - 2 - k + r;
+    if (cb >= L) cb -= L;
+    cb += 1;
+    p = ca;
+    q = cb;
+}
+
+// Pairings M_0..M_{2C-2} (circle method on panel labels) and, between
+// consecutive ones, the exchange in which every CTA keeps one panel: walk
+// each alternating cycle of M_t u M_{t+1}, the CTA keeping vertex v takes
+// the M_{t+1} edge (v, w) and receives w from w's holder, which keeps its
+// other panel.  Checked: every panel pair meets exactly once per sweep.
+static bool build_sched(int C, Sched &s) {
+    const int NP = 2 * C, S = NP - 1;
+    if (C < 2 || C > MAXC) return false;
+    s = Sched{};
+    int hold[MAXC][2];
+    for (int k = 0; k < C; ++k) {
+        pair_host(k, 0, NP, hold[k][0], hold[k][1]);
+        s.ida[0][k] = (signed char)hold[k][0];
+        s.idb[0][k] = (signed char)hold[k][1];
+    }
+    for (int r = 0; r + 1 < S; ++r) {
+        int partner[2 * MAXC], owner[2 * MAXC];
+        for (int k = 0; k < C; ++k) {
+            int p, q;
+            pair_host(k, r + 1, NP, p, q);
+            partner[p] = q;
+            partner[q] = p;
+            owner[hold[k][0]] = k;
+            owner[hold[k][1]] = k;
+        }
+        bool done[MAXC] = {};
+        int nh[MAXC][2];
+        for (int c0 = 0; c0 < C; ++c0) {
+            if (done[c0]) continue;
+            int c = c0, kr = 1;  // CTA c keeps the panel in role kr
+            for (int guard = 0;; ++guard) {
+                if (guard > NP) return false;
+                const int kv = hold[c][kr], w = partner[kv], c2 = owner[w];
+                if (c2 == c || done[c]) return false;
+                nh[c][kr] = kv;
+                nh[c][1 - kr] = w;
+                s.src[r][c] = (signed char)c2;
+                s.dst[r][c2] = (signed char)c;
+                done[c] = true;
+                kr = hold[c2][0] == w ? 1 : 0;  // c2 sends w and keeps its other panel
+                c = c2;
+                if (c == c0) {
+                    if (kr != 1) return false;
+                    break;
+                }
+            }
+        }
+        for (int k = 0; k < C; ++k) {
+            hold[k][0] = nh[k][0];
+            hold[k][1] = nh[k][1];
+            s.ida[r + 1][k] = (signed char)hold[k][0];
+            s.idb[r + 1][k] = (signed char)hold[k][1];
+        }
+    }
+    int seen[2 * MAXC][2 * MAXC] = {};
+    for (int t = 0; t < S; ++t)
+        for (int k = 0; k < C; ++k) {
+            const int x = s.ida[t][k], y = s.idb[t][k];
+            if (x == y) return false;
+            ++seen[x < y ? x : y][x < y ? y : x];
+        }
+    for (int x = 0; x < NP; ++x)
+        for (int y = x + 1; y < NP; ++y)
+            if (seen[x][y] != 1) return false;
+    return true;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
 template <int MR, int NC>
-static int launch(const JacArgs<float> &args0, cudaStream_t st, bool dry, long long *ncl_out) {
+static size_t ws_bytes_for(int ngroups) {
     using K = Cfg<MR, NC>;
-    JacArgs<float> args = args0;
+    return align256((size_t)ngroups * K::C * CT_BYTES) + align256((size_t)ngroups * 2 * NC * sizeof(float)) +
+           (size_t)ngroups * K::C * 2 * K::SLOT;
+}
+
+static int max_groups(int C) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+    return sms / C;  // one CTA per SM (the three panel slots take ~200 KB)
+}
+
+template <int MR, int NC>
+static int launch(const JacArgs<float> &a, void *wsp, size_t wsb, cudaStream_t st) {
+    using K = Cfg<MR, NC>;
+    static Sched sched;
+    static int sched_ok = -1;
+    if (sched_ok < 0) sched_ok = build_sched(K::C, sched) ? 1 : 0;
+    if (!sched_ok) return fail(CS_EINVAL, "tcb SVD: exchange schedule construction failed");
     auto kern = jacobi_tcb_kernel<MR, NC>;
     CS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
+    int per_sm = 0;
+    CS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, K::SMEM));
+    if (per_sm < 1) return fail(CS_ENOMEM, "tcb SVD: kernel does not fit on an SM");
+    const long long ng = lmin(a.count, (long long)max_groups(K::C));
+    if (ng < 1) return CS_OK;
+    const size_t need = ws_bytes_for<MR, NC>(max_groups(K::C));
+    if (!wsp || wsb < need) return fail(CS_ENOMEM, "tcb SVD: workspace too small (query cs_batched_svd_workspace)");
+    unsigned char *base = (unsigned char *)wsp;
+    Ws ws;
+    ws.ctrl = base;
+    ws.gsig = (float *)(base + align256((size_t)ng * K::C * CT_BYTES));
+    ws.mail = (unsigned char *)ws.gsig + align256((size_t)ng * 2 * NC * sizeof(float));
+    ws.ngroups = (int)ng;
+    CS_CUDA_TRY(cudaMemsetAsync(ws.ctrl, 0, (size_t)ng * K::C * CT_BYTES, st));
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = K::C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    attr[0].id = cudaLaunchAttributeCooperative;  // the CTAs of a group must be co-resident
+    attr[0].val.cooperative = 1;
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = K::SMEM;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(K::C);
-    int maxc = 0;
-    CS_CUDA_TRY(cudaOccupancyMaxActiveClusters(&maxc, (void *)kern, &cfg));
-    if (maxc <= 0) return fail(CS_ENOMEM, "tcb SVD: cluster configuration cannot be scheduled");
-    const long long ncl = lmin(args.count, (long long)maxc);
-    if (ncl_out) *ncl_out = ncl;
-    if (dry) return CS_OK;
-    args.s.num_clusters = ncl;
-    cfg.gridDim = dim3((unsigned)(ncl * K::C));
-    CS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args));
+    cfg.gridDim = dim3((unsigned)(ng * K::C));
+    CS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, sched, ws));
     return check_launch("jacobi_tcb_kernel");
 }
 
@@ -619,20 +875,25 @@ static int launch(const JacArgs<float> &args0, cudaStream_t st, bool dry, long l
 // orientation mr x nc, vectors requested, fp32)
 bool tcb_supported(int mr, int nc, bool wantv) { return wantv && mr == 256 && nc == 256; }
 
+size_t tcb_workspace(int mr, int nc, bool wantv) {
+    if (!tcb_supported(mr, nc, wantv)) return 0;
+    return tcb::ws_bytes_for<256, 256>(tcb::max_groups(tcb::Cfg<256, 256>::C));
+}
+
 #ifdef CS_TCB_CLOCKS
 extern "C" int cs_debug_tcb_cycles(unsigned long long *out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return 4;
-    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 10);
+    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 16);
     if (reset) {
-        unsigned long long z[10] = {};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbol(tcb::g_tcb_cycles, z, sizeof(z));
     }
     return 0;
 }
 #endif
 
-int tcb_dispatch(const JacArgs<float> &a, cudaStream_t st) {
-    if (a.s.mr == 256 && a.s.nc == 256) return tcb::launch<256, 256>(a, st, false, nullptr);
+int tcb_dispatch(const JacArgs<float> &a, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (a.s.mr == 256 && a.s.nc == 256) return tcb::launch<256, 256>(a, ws, ws_bytes, st);
     return fail(CS_EINVAL, "tcb SVD: unsupported shape");
 }
 

@@ -11,15 +11,18 @@ dev = torch.device("cuda:0")
 layer = configs.WORKLOADS[5].layers[0]
 wd = torch.from_numpy(configs.layer_weights(layer)).to(dev)
 L = _lib.load()
-buf = (ctypes.c_ulonglong * 10)()
+buf = (ctypes.c_ulonglong * 16)()
 lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 1)
 res = lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 0)
 n = buf[9]
-names = ["gram", "G-read", "angles", "D (rot/exp)", "bop+update", "epi-add", "exch-transfer", "exch-wait"]
+names = ["gram", "G-read", "angles", "D (rot/exp)", "bop+update", "epi-add+V-wait", "exchange (send, recv issue)", "wait incoming X"]
 tot = sum(buf[i] for i in range(8))
 print(f"{count} blocks warm={warm}: {n} super-rounds on CTA thread 0s, sweeps {res.info.float().mean().item():.2f}")
 for i, nm in enumerate(names):
     print(f"  {nm:12s} {buf[i] / n:8.0f} cycles/super-round ({100 * buf[i] / tot:.1f}%)")
 print(f"  total        {tot / n:8.0f}")
+sub = ["ack wait", "store issue+read", "X store complete", "V store complete", "poll partner X", "poll partner V"]
+for i, nm in enumerate(sub):
+    print(f"    {nm:18s} {buf[10 + i] / n:8.0f}")
