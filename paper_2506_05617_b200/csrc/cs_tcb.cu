@@ -50,6 +50,7 @@ namespace cs {
 namespace tcb {
 
 constexpr int NT = 512;
+constexpr int GW = 4;  // Gram-issuing warps (one TMEM accumulator each)
 constexpr int MAXC = 8;
 
 #ifdef CS_TCB_CLOCKS
@@ -102,7 +103,7 @@ struct Cfg {
     static constexpr uint32_t FLAG_OFF = PERM_OFF + 2 * NC * 4;
     static constexpr uint32_t RED_OFF = FLAG_OFF + 16 * 4;
     static constexpr uint32_t BAR_OFF = (RED_OFF + 64 * 4 + 15) & ~15u;
-    static constexpr uint32_t TM_OFF = BAR_OFF + 4 * 8;
+    static constexpr uint32_t TM_OFF = BAR_OFF + 6 * 8;
     static constexpr uint32_t SMEM = TM_OFF + 16;
     static constexpr int STAGES = MR / 64;
     static constexpr int MBLK = ROWS / 128;
@@ -246,9 +247,13 @@ __device__ void expm_minus_identity(float2 *Em, float2 *Tm, float2 *Dm, float *r
 }
 
 // Gram stage: rows [r0, r0+64) of the X rows of the pair (a: real columns
-// 0..31, b: 32..63) -> the transposed hi|lo staging (cs_tcb.cuh gram_stage)
+// 0..31, b: 32..63) -> the transposed hi|lo staging S (cs_tcb.cuh gram_stage)
+// with MN rows ordered [hi_a | lo_a | hi_b | lo_b] (32 each), so the cross
+// block needs only S x [hi_b | lo_b]^T (M = 128, N = 64).  Also accumulates
+// this thread's share of the exact fp32 squared norm of real column
+// tid & 63 (the Gram diagonal).
 __device__ __forceinline__ void gram_stage2(const unsigned char *Pa, const unsigned char *Pb, int r0,
-                                            unsigned char *stg) {
+                                            unsigned char *stg, float &nsq) {
 #pragma unroll
     for (int i = 0; i < 1024 / NT; ++i) {
         const int u = threadIdx.x + i * NT, j = u & 63, rq = u >> 6;
@@ -259,13 +264,15 @@ __device__ __forceinline__ void gram_stage2(const unsigned char *Pa, const unsig
         h.y = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 1, k));
         h.z = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 2, k));
         h.w = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 3, k));
+        nsq = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, nsq))));
         // round-to-nearest split (hi symmetric around x): the dropped lo*lo
         // term is then unbiased
         const float4 hr = make_float4(rna_tf32(h.x), rna_tf32(h.y), rna_tf32(h.z), rna_tf32(h.w));
         const float4 lr = make_float4(rna_tf32(h.x - hr.x), rna_tf32(h.y - hr.y), rna_tf32(h.z - hr.z),
                                       rna_tf32(h.w - hr.w));
-        *reinterpret_cast<float4 *>(stg + sw_chunk(j, rq, 16384)) = hr;
-        *reinterpret_cast<float4 *>(stg + sw_chunk(64 + j, rq, 16384)) = lr;
+        const int hrow = j + (j & 32);  // hi_a 0..31, hi_b 64..95; lo 32 rows further
+        *reinterpret_cast<float4 *>(stg + sw_chunk(hrow, rq, 16384)) = hr;
+        *reinterpret_cast<float4 *>(stg + sw_chunk(hrow + 32, rq, 16384)) = lr;
     }
 }
 
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     int *perm = reinterpret_cast<int *>(sm + K::PERM_OFF);
     int *flags = reinterpret_cast<int *>(sm + K::FLAG_OFF);
     float *red = reinterpret_cast<float *>(sm + K::RED_OFF);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);  // [0,1] MMA ring, [2] X in, [3] V in
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);  // [0,1] update ring, [2] X in, [3] V in, [4,5] Gram ring
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + K::TM_OFF);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -297,15 +304,21 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     }
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        mbar_init(&bar[4], GW);  // one commit per Gram-issuing warp
+        mbar_init(&bar[5], GW);
         fence_mbar_init();
     }
     __syncthreads();
     tc_after_sync();
     const uint32_t tmem = *tmem_slot;
-    uint32_t ph1 = 0, ph2 = 0, phx = 0, phv = 0;  // mbarrier parities (uniform over the CTA)
+    uint32_t ph1 = 0, ph2 = 0, phx = 0, phv = 0, pg0 = 0, pg1 = 0;  // mbarrier parities (CTA-uniform)
     auto ring_wait = [&](int slot) {
         if (slot == 0) { mbar_wait(&bar[0], ph1); ph1 ^= 1; }
         else { mbar_wait(&bar[1], ph2); ph2 ^= 1; }
+    };
+    auto gram_wait = [&](int slot) {
+        if (slot == 0) { mbar_wait(&bar[4], pg0); pg0 ^= 1; }
+        else { mbar_wait(&bar[5], pg1); pg1 ^= 1; }
     };
     unsigned epoch = 0, vseq = 0, mseq = 0;  // exchanges, sweeps, matrices of this launch (group-uniform)
 
@@ -368,68 +381,116 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 float2 *Dm = reinterpret_cast<float2 *>(RG + SC_D);
                 float2 *Gm = reinterpret_cast<float2 *>(RG + SC_G);
                 unsigned char *Bop = RG + SC_BOP;
+                // the exchange after this super-round: outgoing role o, sender src
+                const bool xchg = i < STEPS - 1;
+                const int t2 = xchg ? (fwd ? t + 1 : t - 1) : t;
+                const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;
+                unsigned char *const outbox = box(rank, (epoch + 1) & 1);
+                if (xchg && tid == 0 && epoch + 1 > 2)  // the receiver of epoch-1 consumed this mailbox
+                    spin_ge(myctl + CT_ACK + 4 * ((epoch + 1) & 1), epoch - 1, 1);
                 if (wait_x) {
                     mbar_wait(&bar[2], phx);
                     phx ^= 1;
                     wait_x = false;
                 }
                 TCB_MARK(7);
-                // ---- (1) Gram: STAGES x 64 X rows, transposed hi|lo staging, 2-slot ring
+                // ---- (1) Gram: STAGES x 64 X rows, transposed hi|lo staging, 2-slot ring.
+                // The 8 K-steps of a stage are issued by GW warps (2 each), warp w
+                // accumulating its K-steps of every stage in accumulator w, so GW
+                // MMA streams run side by side.
+                float nsq = 0.f;
 #pragma unroll 1
                 for (int st = 0; st < K::STAGES; ++st) {
                     const int slot = st & 1;
-                    if (st >= 2) ring_wait(slot);
-                    gram_stage2(Pa, Pb, 64 * st, RG + slot * 32768);
+                    if (st >= 2) gram_wait(slot);
+                    gram_stage2(Pa, Pb, 64 * st, RG + slot * 32768, nsq);
                     fence_proxy_async_smem();
                     __syncthreads();
-                    if (warp == (st & 3)) {  // one issuing warp per stage (issuers overlap)
+                    if (warp < GW) {
                         if (lane == 0) {
                             tc_after_sync();
-                            gram_mma(tmem + 128 * (st & 3), smem_u32(RG + slot * 32768));
-                            mma_commit(&bar[slot]);
+                            const uint32_t sa = smem_u32(RG + slot * 32768), d = tmem + 128 * warp;
+#pragma unroll
+                            for (int kk = 0; kk < 8 / GW; ++kk) {
+                                const int ks = warp * (8 / GW) + kk;
+                                const uint32_t o2 = (ks >> 2) * 16384 + (ks & 3) * 32;
+                                const uint32_t acc = (st | kk) ? 1u : 0u;
+                                if (full)  // S S^T: every block (within a, within b, cross)
+                                    mma_tf32(d, desc_sw128(sa + o2), desc_sw128(sa + o2), IDESC_GRAM, acc);
+                                else       // S [hi_b | lo_b]^T: the cross block
+                                    mma_tf32(d, desc_sw128(sa + o2), desc_sw128(sa + 8192 + o2), IDESC_CROSS, acc);
+                            }
+                            mma_commit(&bar[4 + slot]);
                         }
                         __syncwarp();
                     }
                 }
-                if (K::STAGES >= 2) { ring_wait(K::STAGES & 1); ring_wait((K::STAGES + 1) & 1); }
-                else ring_wait(0);
+                reinterpret_cast<float *>(perm)[tid] = nsq;  // column tid & 63, row share tid >> 6
+                if (K::STAGES >= 2) { gram_wait(K::STAGES & 1); gram_wait((K::STAGES + 1) & 1); }
+                else gram_wait(0);
                 tc_after_sync();
                 TCB_MARK(0);
-                // ---- (2) G (complex, 32 x 32) from the stage accumulators: row i < 64
-                // of a 128 x 128 accumulator is TMEM lane i; columns [0, 64) = hi*hi,
-                // [64, 128) = hi*lo.  R = HH + HL + HL^T (real 64 x 64 Gram of the
-                // real columns), summed over stages in fp32.
+                // ---- (2) G (complex, 32 x 32) from the GW accumulators (summed in fp32).
+                // TMEM lane = S row; S rows: hi(i) = i + (i & 32), lo(i) = hi(i) + 32
+                // for real column i.  R = hi*hi + hi*lo + lo*hi.
+                //   full:  T[i][k] = (S S^T)[hi(i)][k], k < 128   (lanes 0..31, 64..95)
+                //          R[i][j] = T[i][hi(j)] + T[i][lo(j)] + T[j][lo(i)]
+                //   cross: T0[i][k] = (S Sb^T)[i][k], k < 64  (hi_a rows, lanes 0..31)
+                //          T1[i][k] = (S Sb^T)[32 + i][k], k < 32 (lo_a rows, lanes 32..63)
+                //          R[i][32 + j] = T0[i][j] + T0[i][32 + j] + T1[i][j]
+                // The diagonal is the exact fp32 column norms from the staging pass.
                 {
-                    float *HH = reinterpret_cast<float *>(RG + SC_HH);
-                    float *HL = reinterpret_cast<float *>(RG + SC_HL);
+                    float *T = reinterpret_cast<float *>(RG);
+                    float *T0 = T, *T1 = T + 32 * 65;
                     const int q = warp & 3, cb = 32 * (warp >> 2);
-                    if (q < 2) {  // lanes 0..63: warps with quarter 0, 1; 32 columns each
+                    const bool act_rd = full ? (q == 0 || q == 2) : ((q == 0 && cb < 64) || (q == 1 && cb == 0));
+                    if (act_rd) {
                         float acc[32];
 #pragma unroll
                         for (int i2 = 0; i2 < 32; ++i2) acc[i2] = 0.f;
 #pragma unroll 1
-                        for (int st = 0; st < K::STAGES; ++st) {
-                            float v[16];
-                            tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * st + cb, v);
+                        for (int w = 0; w < GW; ++w) {
+                            float v[16], w2[16];
+                            tmem_ld16x2s(tmem + ((uint32_t)(32 * q) << 16) + 128 * w + cb, v, w2);
 #pragma unroll
-                            for (int i2 = 0; i2 < 16; ++i2) acc[i2] += v[i2];
-                            tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * st + cb + 16, v);
-#pragma unroll
-                            for (int i2 = 0; i2 < 16; ++i2) acc[16 + i2] += v[i2];
+                            for (int i2 = 0; i2 < 16; ++i2) { acc[i2] += v[i2]; acc[16 + i2] += w2[i2]; }
                         }
-                        const int row = 32 * q + lane;
-                        float *dstp = cb < 64 ? HH + row * LDR + cb : HL + row * LDR + (cb - 64);
+                        float *dstp = full ? T + ((q == 0 ? 0 : 32) + lane) * 129 + cb
+                                           : (q == 0 ? T0 + lane * 65 + cb : T1 + lane * 33);
 #pragma unroll
                         for (int i2 = 0; i2 < 32; ++i2) dstp[i2] = acc[i2];
                     }
                     tc_before_sync();
                     __syncthreads();
-                    for (int x = tid; x < N2 * N2; x += NT) {
-                        const int c = x >> 5, j = x & 31;
-                        auto R = [&](int i2, int k) { return HH[i2 * LDR + k] + HL[i2 * LDR + k] + HL[k * LDR + i2]; };
-                        // G_r = R[2c][2j] + R[2c+1][2j+1], G_i = R[2c][2j+1] - R[2c+1][2j]
-                        Gm[c * LDG + j] = make_float2(R(2 * c, 2 * j) + R(2 * c + 1, 2 * j + 1),
-                                                      R(2 * c, 2 * j + 1) - R(2 * c + 1, 2 * j));
+                    const float *part = reinterpret_cast<const float *>(perm);
+                    auto nrm = [&](int j) {
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int k = 0; k < NT / 64; ++k) sacc += part[j + 64 * k];
+                        return sacc;
+                    };
+                    if (full) {
+                        auto hi = [](int i) { return i + (i & 32); };
+                        auto R = [&](int i2, int k) {
+                            return T[i2 * 129 + hi(k)] + T[i2 * 129 + hi(k) + 32] + T[k * 129 + hi(i2) + 32];
+                        };
+                        for (int x = tid; x < N2 * N2; x += NT) {
+                            const int c = x >> 5, j = x & 31;
+                            // G_r = R[2c][2j] + R[2c+1][2j+1], G_i = R[2c][2j+1] - R[2c+1][2j]
+                            Gm[c * LDG + j] = c == j ? make_float2(nrm(2 * c) + nrm(2 * c + 1), 0.f)
+                                                     : make_float2(R(2 * c, 2 * j) + R(2 * c + 1, 2 * j + 1),
+                                                                   R(2 * c, 2 * j + 1) - R(2 * c + 1, 2 * j));
+                        }
+                    } else {
+                        auto R = [&](int i2, int k) { return T0[i2 * 65 + k] + T0[i2 * 65 + 32 + k] + T1[i2 * 33 + k]; };
+                        if (tid < W * W) {
+                            const int c = tid >> 4, d = tid & 15;
+                            Gm[c * LDG + W + d] = make_float2(R(2 * c, 2 * d) + R(2 * c + 1, 2 * d + 1),
+                                                              R(2 * c, 2 * d + 1) - R(2 * c + 1, 2 * d));
+                        } else if (tid < W * W + N2) {
+                            const int c = tid - W * W;
+                            Gm[c * LDG + c] = make_float2(nrm(2 * c) + nrm(2 * c + 1), 0.f);
+                        }
                     }
                     __syncthreads();
                 }
@@ -510,116 +571,106 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     build_bop<NT>(Dm, Bop);
                     finish_v();       // the V rows of an incoming panel are needed from here
                     __syncthreads();  // D read before the ring (aliasing it) is written
-#pragma unroll 1
-                    for (int ch = 0; ch < 2 * K::MBLK; ++ch) {
-                        const int mb = ch >> 1, at = ch & 1, slot = ch & 1;
-                        if (ch >= 2) ring_wait(slot);
-                        unsigned char *lo = RG + slot * 16384;
-                        const unsigned char *srcp = (at ? Pb : Pa) + mb * 16384;
+                    // software pipeline over the 128-row M-blocks: stage lo(P) of block
+                    // mb (both panels, the two 16 KB ring slots), issue its MMAs, then
+                    // apply block mb-1's accumulator while the tensor core runs block mb
+                    // (its MMAs read the hi words straight from the panels, so block
+                    // mb-1's rows are rewritten only after its MMAs completed).  Each
+                    // block's MMA stream comes from its own warp: one warp's stream
+                    // completes ~285 cycles per MMA, streams of different warps overlap
+                    // (tools/tc_rate_probe.cu).
+                    auto epi = [&](int mb) {
+                        // quarter q = TMEM lanes (rows), warp group c = 16 output real columns
+                        const int q = warp & 3, c = warp >> 2;
+                        const int row = mb * 128 + 32 * q + lane;
+                        float v[16], vc[16];
+                        tmem_ld16x2(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 16 * c, v, vc);
 #pragma unroll
-                        for (int i2 = 0; i2 < 1024 / NT; ++i2) {
-                            const int u = tid + i2 * NT;
-                            *reinterpret_cast<float4 *>(lo + 16 * u) =
-                                lo4(*reinterpret_cast<const float4 *>(srcp + 16 * u));
+                        for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int k4 = 4 * c + u, role = k4 >> 3;
+                            const uint32_t off = so4(row, k4 & 7);
+                            float4 *pp = reinterpret_cast<float4 *>((role ? Pb : Pa) + off);
+                            float4 x = *pp;
+                            x.x += v[4 * u]; x.y += v[4 * u + 1]; x.z += v[4 * u + 2]; x.w += v[4 * u + 3];
+                            // the outgoing panel goes straight to the mailbox (same layout)
+                            if (xchg && role == o) __stcg(reinterpret_cast<float4 *>(outbox + off), x);
+                            else *pp = x;
+                        }
+                    };
+#pragma unroll 1
+                    for (int mb = 0; mb < K::MBLK; ++mb) {
+                        if (mb >= 1) {
+                            ring_wait((mb - 1) & 1);  // block mb-1 done: lo slots free, accumulator ready
+                            tc_after_sync();
+                        }
+#pragma unroll
+                        for (int i2 = 0; i2 < 2048 / NT; ++i2) {
+                            const int u = tid + i2 * NT, at = u >> 10, w = u & 1023;
+                            *reinterpret_cast<float4 *>(RG + at * 16384 + 16 * w) =
+                                lo4(*reinterpret_cast<const float4 *>((at ? Pb : Pa) + mb * 16384 + 16 * w));
                         }
                         fence_proxy_async_smem();
                         __syncthreads();
-                        if (warp == 4 + slot) {  // one issuing warp per ring slot
+                        if (warp == (mb & 3)) {
                             if (lane == 0) {
                                 tc_after_sync();
                                 const uint32_t d = tmem + 128 * mb;
-                                const uint32_t ah = smem_u32(srcp), al = smem_u32(lo);
-                                const uint32_t bb = smem_u32(Bop) + at * 16384;
 #pragma unroll
-                                for (int ks = 0; ks < 4; ++ks) {
-                                    const uint64_t dah = desc_sw128(ah + ks * 32), dal = desc_sw128(al + ks * 32);
-                                    const uint64_t db = desc_sw128(bb + ks * 32);
-                                    const uint32_t acc0 = (at | ks) ? 1u : 0u;
-                                    mma_tf32(d, dah, db, IDESC_UPD, acc0);          // [hi*hi | hi*lo]
-                                    mma_tf32(d + 64, dal, db, IDESC_UPD_LO, 1u);    // + lo*hi -> correction
+                                for (int at = 0; at < 2; ++at) {
+                                    const uint32_t ah = smem_u32((at ? Pb : Pa) + mb * 16384);
+                                    const uint32_t al = smem_u32(RG + at * 16384);
+                                    const uint32_t bb = smem_u32(Bop) + at * 16384;
+#pragma unroll
+                                    for (int ks = 0; ks < 4; ++ks) {
+                                        const uint64_t dah = desc_sw128(ah + ks * 32), dal = desc_sw128(al + ks * 32);
+                                        const uint64_t db = desc_sw128(bb + ks * 32);
+                                        const uint32_t acc0 = (at | ks) ? 1u : 0u;
+                                        mma_tf32(d, dah, db, IDESC_UPD, acc0);        // [hi*hi | hi*lo]
+                                        mma_tf32(d + 64, dal, db, IDESC_UPD_LO, 1u);  // + lo*hi -> correction
+                                    }
                                 }
-                                mma_commit(&bar[slot]);
+                                mma_commit(&bar[mb & 1]);
                             }
                             __syncwarp();
                         }
+                        if (mb >= 1) epi(mb - 1);
                     }
-                    ring_wait(0);
-                    ring_wait(1);
+                    ring_wait((K::MBLK - 1) & 1);
                     tc_after_sync();
                     TCB_MARK(4);
-                    // ---- (7) P += acc: warp group -> M-blocks, quarter q -> lanes;
-                    // output real column n -> chunk n/4 of panel a (n < 32) or b
-                    {
-                        const int q = warp & 3;
-#pragma unroll 1
-                        for (int mb = warp >> 2; mb < K::MBLK; mb += NT / 128) {
-                            const int row = mb * 128 + 32 * q + lane;
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                float v[16], vc[16];
-                                tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 16 * c, v);
-                                tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 64 + 16 * c, vc);
-#pragma unroll
-                                for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const int k4 = 4 * c + u;
-                                    float4 *pp = reinterpret_cast<float4 *>((k4 < 8 ? Pa : Pb) + so4(row, k4 & 7));
-                                    float4 x = *pp;
-                                    x.x += v[4 * u]; x.y += v[4 * u + 1]; x.z += v[4 * u + 2]; x.w += v[4 * u + 3];
-                                    *pp = x;
-                                }
-                            }
-                        }
-                        tc_before_sync();
-                    }
+                    epi(K::MBLK - 1);
+                    tc_before_sync();
                 }
                 finish_v();
-                fence_proxy_async_smem();  // panel writes -> the TMA store of the outgoing panel
-                __syncthreads();
                 TCB_MARK(5);
                 // ---- (8) exchange to the next pairing: keep one panel, send the other
-                // to dst's mailbox, receive the new one from src's into the scratch slot
-                if (i < STEPS - 1) {
-                    const int t2 = fwd ? t + 1 : t - 1;
-                    const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;  // outgoing role
+                // to dst through this CTA's mailbox (written by the epilogue above
+                // when the pair rotated, copied here otherwise), receive the new one
+                // from src's mailbox into the scratch slot
+                if (xchg) {
                     const int src = fwd ? sc.src[t][rank] : sc.dst[t2][rank];
+                    if (!(any_rot && !bad)) {
+                        const float4 *sp = reinterpret_cast<const float4 *>(sm + sl[o] * SLOT);
+                        float4 *dp = reinterpret_cast<float4 *>(outbox);
+#pragma unroll 4
+                        for (int u = tid; u < (int)(SLOT / 16); u += NT) __stcg(dp + u, sp[u]);
+                    }
                     ++epoch;
-                    const int par = epoch & 1;
+                    __threadfence();
+                    __syncthreads();
                     if (tid == 0) {
-#ifdef CS_TCB_CLOCKS
-                        long long tcb_s = clock64();
-#endif
-                        if (epoch > 2) spin_ge(myctl + CT_ACK + 4 * par, epoch - 2, 1);  // mailbox consumed
-                        TCB_SUB(10);
-                        unsigned char *mb = box(rank, par);
-                        const uint32_t os = smem_u32(sm + sl[o] * SLOT);
-                        bulk_s2g(mb, os, XBYTES);
-                        bulk_commit();
-                        bulk_s2g(mb + XBYTES, os + XBYTES, SLOT - XBYTES);
-                        bulk_commit();
-                        bulk_wait_read_all();  // the outgoing slot is free (next scratch)
-                        TCB_SUB(11);
-                        bulk_wait_but1();
                         fence_proxy_async_global();
                         st_rel(myctl + CT_FX, epoch);
-                        TCB_SUB(12);
-                        bulk_wait_all();
-                        fence_proxy_async_global();
-                        st_rel(myctl + CT_FV, epoch);
-                        TCB_SUB(13);
-                        const unsigned char *in = box(src, par);
+                        const unsigned char *in = box(src, epoch & 1);
                         const uint32_t is = smem_u32(sm + sl[2] * SLOT);
                         spin_ge(ctl(src) + CT_FX, epoch, 2);
                         fence_proxy_async_global();
                         mbar_arrive_expect_tx(&bar[2], XBYTES);
                         bulk_g2s(is, in, XBYTES, smem_u32(&bar[2]));
-                        TCB_SUB(14);
-                        spin_ge(ctl(src) + CT_FV, epoch, 3);
-                        fence_proxy_async_global();
                         mbar_arrive_expect_tx(&bar[3], SLOT - XBYTES);
                         bulk_g2s(is + XBYTES, in + XBYTES, SLOT - XBYTES, smem_u32(&bar[3]));
-                        TCB_SUB(15);
                     }
                     wait_x = wait_v = true;
                     src_pending = src;
@@ -628,6 +679,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     sl[o] = ns;
                     ia = sc.ida[t2][rank];
                     ib = sc.idb[t2][rank];
+                    __syncthreads();
+                } else {
                     __syncthreads();
                 }
                 TCB_MARK(6);

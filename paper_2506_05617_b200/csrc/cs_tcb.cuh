@@ -51,6 +51,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 constexpr uint32_t IDESC_GRAM = idesc_tf32(128, 128);
+constexpr uint32_t IDESC_CROSS = idesc_tf32(128, 64);  // S x [hi_b | lo_b]^T
 constexpr uint32_t IDESC_UPD = idesc_tf32(128, 128);   // hi(P) x [hi(D); lo(D)]
 constexpr uint32_t IDESC_UPD_LO = idesc_tf32(128, 64); // lo(P) x hi(D)
 
@@ -76,6 +77,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// two 32x32b.x16 loads (columns c and c + OFF of the same lanes) under one wait
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16_pair(uint32_t addr, float (&v)[16], float (&w)[16]) {
+    uint32_t r[16], q[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+          "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15])
+        : "r"(addr + OFF));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        v[i] = __uint_as_float(r[i]);
+        w[i] = __uint_as_float(q[i]);
+    }
+}
+__device__ __forceinline__ void tmem_ld16x2(uint32_t addr, float (&v)[16], float (&w)[16]) {
+    tmem_ld16_pair<64>(addr, v, w);
+}
+__device__ __forceinline__ void tmem_ld16x2s(uint32_t addr, float (&v)[16], float (&w)[16]) {
+    tmem_ld16_pair<16>(addr, v, w);
 }
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 // tf32 round-to-nearest (the residual of hi = trunc(x) has 13 significant

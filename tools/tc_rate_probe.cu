@@ -57,7 +57,13 @@ int main() {
     cudaMalloc(&d, 8 * 148);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
     int cases[][6] = {{128, 1, 64, 96, 0, 1}, {128, 1, 64, 96, 0, 2}, {128, 1, 64, 96, 0, 4},
-                      {64, 1, 64, 96, 0, 1}, {64, 1, 64, 96, 0, 4}, {128, 1, 256, 96, 0, 1}, {128, 1, 256, 96, 0, 2}};
+                      {64, 1, 64, 96, 0, 1}, {64, 1, 64, 96, 0, 4}, {128, 1, 256, 96, 0, 1}, {128, 1, 256, 96, 0, 2},
+                      // latency of the Jacobi's small batches: 1 and 8 MMAs issue -> commit -> mbarrier
+                      {128, 1, 64, 1, 0, 1}, {128, 1, 64, 8, 0, 1}, {128, 1, 128, 8, 0, 1}, {128, 1, 128, 32, 0, 1},
+                      {128, 1, 128, 96, 0, 1},
+                      // one issuing warp, independent accumulators round-robin
+                      {128, 2, 64, 96, 0, 1}, {128, 4, 64, 96, 0, 1}, {128, 4, 128, 96, 0, 1}, {128, 4, 64, 8, 0, 1},
+                      {128, 8, 64, 96, 0, 1}, {128, 4, 64, 32, 0, 1}};
     for (auto &c : cases) {
         k<<<148, 128, 65536>>>(d, c[0], c[1], c[2], c[3], c[4], c[5]);
         cudaError_t e = cudaDeviceSynchronize();

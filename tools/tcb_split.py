@@ -17,12 +17,12 @@ L.cs_debug_tcb_cycles(buf, 1)
 res = lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 0)
 n = buf[9]
-names = ["gram", "G-read", "angles", "D (rot/exp)", "bop+update", "epi-add+V-wait", "exchange (send, recv issue)", "wait incoming X"]
+names = ["gram", "G-read", "angles", "D (rot/exp)", "bop+update", "epi-add+V-wait", "exchange", "wait incoming X"]
 tot = sum(buf[i] for i in range(8))
 print(f"{count} blocks warm={warm}: {n} super-rounds on CTA thread 0s, sweeps {res.info.float().mean().item():.2f}")
 for i, nm in enumerate(names):
     print(f"  {nm:12s} {buf[i] / n:8.0f} cycles/super-round ({100 * buf[i] / tot:.1f}%)")
 print(f"  total        {tot / n:8.0f}")
-sub = ["ack wait", "store issue+read", "X store complete", "V store complete", "poll partner X", "poll partner V"]
+sub = ["gram ring wait", "gram staging", "gram fence", "gram syncthreads", "gram issue(t0)", "gram final waits"]
 for i, nm in enumerate(sub):
     print(f"    {nm:18s} {buf[10 + i] / n:8.0f}")
