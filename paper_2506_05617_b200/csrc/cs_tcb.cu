@@ -56,7 +56,7 @@ constexpr int MAXC = 8;
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
-__device__ unsigned long long g_tcb_cycles[16];  // [9] super-round count, [10..15] exchange sub-steps
+__device__ unsigned long long g_tcb_cycles[16];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
         if (tid == 0) {                                                              \
@@ -65,15 +65,13 @@ __device__ unsigned long long g_tcb_cycles[16];  // [9] super-round count, [10..
             tcb_t = _c;                                                              \
         }                                                                            \
     } while (0)
-#define TCB_SUB(i)                                                                   \
+#define TCB_ADD(i, t0)                                                               \
     do {                                                                             \
-        const long long _c = clock64();                                              \
-        atomicAdd(&g_tcb_cycles[i], (unsigned long long)(_c - tcb_s));               \
-        tcb_s = _c;                                                                  \
+        if (tid == 0) atomicAdd(&g_tcb_cycles[i], (unsigned long long)(clock64() - (t0))); \
     } while (0)
 #else
 #define TCB_MARK(i) do { } while (0)
-#define TCB_SUB(i) do { } while (0)
+#define TCB_ADD(i, t0) do { } while (0)
 #endif
 
 // the sweep's pairings and the exchange between consecutive ones (host-built)
@@ -86,10 +84,16 @@ struct Sched {
 struct Ws {
     unsigned char *ctrl;  // per CTA 256 B: flags (see CT_*)
     float *gsig;          // per group [2][NC] squared column norms (epilogue)
-    unsigned char *mail;  // per CTA [2] outgoing panels
+    unsigned char *mail;  // per CTA [NBOX] outgoing panels
     int ngroups;
 };
-constexpr int CT_FX = 0, CT_FV = 32, CT_ACK = 64, CT_VERD = 96, CT_EPI = 160, CT_BYTES = 256;  // ACK/VERD/EPI: [2] by parity
+constexpr int CT_FX = 0, CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_BYTES = 256;  // VERD/EPI/WORK: [2] by parity
+// mailboxes per CTA: exchange e writes mailbox e % NBOX.  A sweep has 2C-2
+// exchanges and ends with a group-wide verdict barrier, so a mailbox is
+// rewritten (NBOX >= 2C-1 exchanges later) only after every CTA of the group
+// passed a verdict that its receiver posted after consuming it: no
+// acknowledgement flags are needed.
+constexpr int NBOX = 16;
 
 template <int MR, int NC>
 struct Cfg {
@@ -103,7 +107,7 @@ struct Cfg {
     static constexpr uint32_t FLAG_OFF = PERM_OFF + 2 * NC * 4;
     static constexpr uint32_t RED_OFF = FLAG_OFF + 16 * 4;
     static constexpr uint32_t BAR_OFF = (RED_OFF + 64 * 4 + 15) & ~15u;
-    static constexpr uint32_t TM_OFF = BAR_OFF + 6 * 8;
+    static constexpr uint32_t TM_OFF = BAR_OFF + 10 * 8;
     static constexpr uint32_t SMEM = TM_OFF + 16;
     static constexpr int STAGES = MR / 64;
     static constexpr int MBLK = ROWS / 128;
@@ -111,6 +115,7 @@ struct Cfg {
     static_assert(SLOT >= 65536, "tcb scratch slot holds the 64 KB Gram/update staging");
     static_assert(STAGES <= 4 && MBLK <= 4, "tcb TMEM budget (4 accumulators of 128 columns)");
     static_assert(C >= 2 && C <= MAXC, "tcb group size");
+    static_assert(NBOX >= 2 * C - 1, "mailbox reuse must cross a sweep-verdict barrier");
     static_assert(SMEM <= 227 * 1024, "tcb shared memory");
 };
 
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     int *perm = reinterpret_cast<int *>(sm + K::PERM_OFF);
     int *flags = reinterpret_cast<int *>(sm + K::FLAG_OFF);
     float *red = reinterpret_cast<float *>(sm + K::RED_OFF);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);  // [0,1] update ring, [2] X in, [3] V in, [4,5] Gram ring
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + K::BAR_OFF);  // [0,1] update ring, [3] V in, [4,5] Gram ring, [6..9] X in by stage
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + K::TM_OFF);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -294,7 +299,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     const float tol = a.tol;
     unsigned char *const myctl = ws.ctrl + (size_t)blockIdx.x * CT_BYTES;
     auto ctl = [&](int cta) { return ws.ctrl + ((size_t)g * C + cta) * CT_BYTES; };
-    auto box = [&](int cta, int par) { return ws.mail + (((size_t)g * C + cta) * 2 + par) * SLOT; };
+    auto box = [&](int cta, int e) { return ws.mail + (((size_t)g * C + cta) * NBOX + (e % NBOX)) * SLOT; };
     float *const gsig = ws.gsig + (size_t)g * 2 * NC;
 
     if (warp == 0) {
@@ -304,6 +309,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     }
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        for (int i = 6; i < 10; ++i) mbar_init(&bar[i], 1);
         mbar_init(&bar[4], GW);  // one commit per Gram-issuing warp
         mbar_init(&bar[5], GW);
         fence_mbar_init();
@@ -322,16 +328,58 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     };
     unsigned epoch = 0, vseq = 0, mseq = 0;  // exchanges, sweeps, matrices of this launch (group-uniform)
 
-    for (long long f = g; f < a.count; f += ws.ngroups) {
+    // dynamic schedule: the group's rank 0 takes the next matrix from a
+    // launch-wide counter (sweep counts differ per matrix) and publishes it
+    // to the group, tagged with the matrix sequence number
+    unsigned *const next = reinterpret_cast<unsigned *>(ws.ctrl + (size_t)gridDim.x * CT_BYTES);
+    for (;;) {
+        if (tid == 0) {
+            const unsigned slot = CT_WORK + 8 * ((mseq + 1) & 1);
+            unsigned long long v;
+            if (rank == 0) {
+                const unsigned fi = atomicAdd(next, 1u);
+                v = ((unsigned long long)(mseq + 1) << 32) | fi;
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(ctl(0) + slot), "l"(v) : "memory");
+            } else {
+                unsigned n = 0;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctl(0) + slot) : "memory");
+                    if ((unsigned)(v >> 32) == mseq + 1) break;
+                    if (++n > (1u << 25)) spin_timeout(6);
+                    __nanosleep(32);
+                }
+            }
+            flags[2] = (int)(unsigned)v;
+        }
+        __syncthreads();
+        const long long f = (unsigned)flags[2];
+        __syncthreads();
+        if (f >= a.count) break;
         const long long mid = a.index ? a.index[f] : f;
         ++mseq;
         int sl[3] = {0, 1, 2};  // slots of panel a, panel b, scratch
         int ia = sc.ida[0][rank], ib = sc.idb[0][rank];
+#ifdef CS_TCB_CLOCKS
+        long long tcb_m = clock64();
+        if (tid == 0) atomicAdd(&g_tcb_cycles[13], 1ull);
+#else
+        long long tcb_m = 0;
+#endif
         // ---- load the two panels (panel x = working columns [x W, x W + W))
         {
             const float2 *X0 = a.initX ? a.initX + (size_t)f * MR * NC : nullptr;
             const float2 *V0 = a.initV ? a.initV + (size_t)a.initV_index[f] * NC * NC : nullptr;
             const float2 *A = a.blocks + (size_t)mid * a.co * a.ci;
+            if (X0 && V0) {  // warm start: 16-byte loads (two complex columns), 16 in flight per thread
+#pragma unroll 16
+                for (int u = tid; u < 2 * K::ROWS * (W / 2); u += NT) {
+                    const int half = u / (K::ROWS * (W / 2)), e = u % (K::ROWS * (W / 2));
+                    const int r = e / (W / 2), j2 = e % (W / 2), j = (half == 0 ? ia : ib) * W + 2 * j2;
+                    const float4 v = r < MR ? __ldg(reinterpret_cast<const float4 *>(X0 + (size_t)r * NC + j))
+                                            : __ldg(reinterpret_cast<const float4 *>(V0 + (size_t)(r - MR) * NC + j));
+                    *reinterpret_cast<float4 *>(sm + sl[half] * SLOT + so4(r, j2)) = v;
+                }
+            } else
             for (int half = 0; half < 2; ++half) {
                 const int c0 = (half == 0 ? ia : ib) * W;
                 unsigned char *P = sm + sl[half] * SLOT;
@@ -353,6 +401,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         }
         __syncthreads();
 
+        TCB_ADD(10, tcb_m);
         int info = -1;
         bool wait_x = false, wait_v = false;  // incoming panel (in flight into slot a or b)
         int src_pending = 0;
@@ -361,7 +410,6 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 mbar_wait(&bar[3], phv);
                 phv ^= 1;
                 wait_v = false;
-                if (tid == 0) st_rel(ctl(src_pending) + CT_ACK + 4 * (epoch & 1), epoch);
             }
         };
         for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
@@ -385,14 +433,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const bool xchg = i < STEPS - 1;
                 const int t2 = xchg ? (fwd ? t + 1 : t - 1) : t;
                 const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;
-                unsigned char *const outbox = box(rank, (epoch + 1) & 1);
-                if (xchg && tid == 0 && epoch + 1 > 2)  // the receiver of epoch-1 consumed this mailbox
-                    spin_ge(myctl + CT_ACK + 4 * ((epoch + 1) & 1), epoch - 1, 1);
-                if (wait_x) {
-                    mbar_wait(&bar[2], phx);
-                    phx ^= 1;
-                    wait_x = false;
-                }
+                unsigned char *const outbox = box(rank, epoch + 1);
+
                 TCB_MARK(7);
                 // ---- (1) Gram: STAGES x 64 X rows, transposed hi|lo staging, 2-slot ring.
                 // The 8 K-steps of a stage are issued by GW warps (2 each), warp w
@@ -403,6 +445,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 for (int st = 0; st < K::STAGES; ++st) {
                     const int slot = st & 1;
                     if (st >= 2) gram_wait(slot);
+                    if (wait_x) mbar_wait(&bar[6 + st], phx);  // the incoming panel's rows of this stage
                     gram_stage2(Pa, Pb, 64 * st, RG + slot * 32768, nsq);
                     fence_proxy_async_smem();
                     __syncthreads();
@@ -426,6 +469,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     }
                 }
                 reinterpret_cast<float *>(perm)[tid] = nsq;  // column tid & 63, row share tid >> 6
+                if (wait_x) {
+                    phx ^= 1;
+                    wait_x = false;
+                }
                 if (K::STAGES >= 2) { gram_wait(K::STAGES & 1); gram_wait((K::STAGES + 1) & 1); }
                 else gram_wait(0);
                 tc_after_sync();
@@ -524,22 +571,46 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         // rotations, D <- D J_r + (J_r - I).  Rows evolve independently,
                         // so the 16 threads of a row (half a warp) only sync warp-wide.
                         const int i2 = tid >> 4, k = tid & 15;
+                        if (!full) {
+                            // cross rounds: slot k pairs a-column k with b-column (k + r) mod W.
+                            // Lane k of row i2's half-warp keeps D[i2][k] and the b-column of
+                            // its current pair in registers; the b-columns move one lane down
+                            // per round (after W rounds every lane holds its own again).
+                            float2 x = make_float2(0.f, 0.f), y = x;
 #pragma unroll 1
-                        for (int r = 0; r < nround; ++r) {
-                            const Prm<float> pm = prm[r * W + k];
-                            if (pm.act > 0) {
-                                int p, qq;
-                                inner_pair(full, k, r, p, qq);
-                                float2 x = Dm[i2 * LDG + p], y = Dm[i2 * LDG + qq];
-                                Rot<float> R;
-                                R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
-                                rot_apply<float>(x, y, R);
-                                if (i2 == p) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
-                                if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
-                                Dm[i2 * LDG + p] = x;
-                                Dm[i2 * LDG + qq] = y;
+                            for (int r = 0; r < W; ++r) {
+                                const Prm<float> pm = prm[r * W + k];
+                                if (pm.act > 0) {
+                                    const int qq = W + ((k + r) & (W - 1));
+                                    Rot<float> R;
+                                    R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                                    rot_apply<float>(x, y, R);
+                                    if (i2 == k) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
+                                    if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
+                                }
+                                y.x = __shfl_sync(0xffffffffu, y.x, (k + 1) & (W - 1), W);
+                                y.y = __shfl_sync(0xffffffffu, y.y, (k + 1) & (W - 1), W);
                             }
-                            __syncwarp();
+                            Dm[i2 * LDG + k] = x;
+                            Dm[i2 * LDG + W + k] = y;
+                        } else {
+#pragma unroll 1
+                            for (int r = 0; r < nround; ++r) {
+                                const Prm<float> pm = prm[r * W + k];
+                                if (pm.act > 0) {
+                                    int p, qq;
+                                    inner_pair(full, k, r, p, qq);
+                                    float2 x = Dm[i2 * LDG + p], y = Dm[i2 * LDG + qq];
+                                    Rot<float> R;
+                                    R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                                    rot_apply<float>(x, y, R);
+                                    if (i2 == p) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
+                                    if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
+                                    Dm[i2 * LDG + p] = x;
+                                    Dm[i2 * LDG + qq] = y;
+                                }
+                                __syncwarp();
+                            }
                         }
                         __syncthreads();
                     } else {
@@ -658,17 +729,23 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         for (int u = tid; u < (int)(SLOT / 16); u += NT) __stcg(dp + u, sp[u]);
                     }
                     ++epoch;
-                    __threadfence();
                     __syncthreads();
                     if (tid == 0) {
+                        // one gpu-scope fence after the CTA barrier publishes every
+                        // thread's mailbox stores (the cooperative-groups grid-sync pattern)
+                        __threadfence();
                         fence_proxy_async_global();
                         st_rel(myctl + CT_FX, epoch);
-                        const unsigned char *in = box(src, epoch & 1);
+                        const unsigned char *in = box(src, epoch);
                         const uint32_t is = smem_u32(sm + sl[2] * SLOT);
                         spin_ge(ctl(src) + CT_FX, epoch, 2);
                         fence_proxy_async_global();
-                        mbar_arrive_expect_tx(&bar[2], XBYTES);
-                        bulk_g2s(is, in, XBYTES, smem_u32(&bar[2]));
+                        constexpr uint32_t XC = XBYTES / K::STAGES;  // the X rows of one Gram stage
+#pragma unroll
+                        for (int c = 0; c < K::STAGES; ++c) {
+                            mbar_arrive_expect_tx(&bar[6 + c], XC);
+                            bulk_g2s(is + c * XC, in + c * XC, XC, smem_u32(&bar[6 + c]));
+                        }
                         mbar_arrive_expect_tx(&bar[3], SLOT - XBYTES);
                         bulk_g2s(is + XBYTES, in + XBYTES, SLOT - XBYTES, smem_u32(&bar[3]));
                     }
@@ -686,6 +763,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 TCB_MARK(6);
             }
             // ---- sweep verdict, OR-ed over the group (double-buffered by sweep parity)
+#ifdef CS_TCB_CLOCKS
+            tcb_m = clock64();
+#endif
             ++vseq;
             if (tid == 0) {
                 st_rel(myctl + CT_VERD + 4 * (vseq & 1), (vseq << 2) | (bad ? 2u : 0u) | (rot ? 1u : 0u));
@@ -697,6 +777,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
             __syncthreads();
             const int any_rot = flags[0], any_bad = flags[1];
             __syncthreads();
+            TCB_ADD(11, tcb_m);
             if (any_bad) break;
             if (!any_rot) {
                 info = sweep + 1;
@@ -704,6 +785,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
             }
         }
 
+#ifdef CS_TCB_CLOCKS
+        tcb_m = clock64();
+#endif
         // ---- epilogue: exact fp32 column norms of the local panels, gathered
         // over the group through global memory; stable descending order;
         // U = X / sigma, V
@@ -779,6 +863,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
             a.zero_sigma[mid] = z;
         }
         __syncthreads();
+        TCB_ADD(12, tcb_m);
     }
     tc_before_sync();
     __syncthreads();
@@ -873,8 +958,8 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 template <int MR, int NC>
 static size_t ws_bytes_for(int ngroups) {
     using K = Cfg<MR, NC>;
-    return align256((size_t)ngroups * K::C * CT_BYTES) + align256((size_t)ngroups * 2 * NC * sizeof(float)) +
-           (size_t)ngroups * K::C * 2 * K::SLOT;
+    return align256((size_t)ngroups * K::C * CT_BYTES + 256) + align256((size_t)ngroups * 2 * NC * sizeof(float)) +
+           (size_t)ngroups * K::C * NBOX * K::SLOT;
 }
 
 static int max_groups(int C) {
@@ -904,10 +989,10 @@ static int launch(const JacArgs<float> &a, void *wsp, size_t wsb, cudaStream_t s
     unsigned char *base = (unsigned char *)wsp;
     Ws ws;
     ws.ctrl = base;
-    ws.gsig = (float *)(base + align256((size_t)ng * K::C * CT_BYTES));
+    ws.gsig = (float *)(base + align256((size_t)ng * K::C * CT_BYTES + 256));
     ws.mail = (unsigned char *)ws.gsig + align256((size_t)ng * 2 * NC * sizeof(float));
     ws.ngroups = (int)ng;
-    CS_CUDA_TRY(cudaMemsetAsync(ws.ctrl, 0, (size_t)ng * K::C * CT_BYTES, st));
+    CS_CUDA_TRY(cudaMemsetAsync(ws.ctrl, 0, (size_t)ng * K::C * CT_BYTES + 256, st));  // flags + work counter
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;  // the CTAs of a group must be co-resident

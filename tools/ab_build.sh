@@ -17,9 +17,11 @@ if [ -n "$REV" ]; then
 fi
 NV=/usr/local/cuda/bin/nvcc
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $CS_AB_FLAGS"
+pids=()
 for f in $(cd "$T/pkg/csrc" && ls *.cu | sed "s/\.cu$//"); do
   $NV $FL -c "$T/pkg/csrc/$f.cu" -o "$T/obj/$f.o" &
+  pids+=($!)
 done
-wait
+for p in "${pids[@]}"; do wait "$p" || { echo "ab_build: a compile failed" >&2; exit 1; }; done
 $NV -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$ROOT/ab_libs/lib$NAME.so" "$T"/obj/*.o -lcufft -Xlinker -rpath,/usr/local/cuda/lib64
 echo "built ab_libs/lib$NAME.so"

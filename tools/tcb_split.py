@@ -23,6 +23,6 @@ print(f"{count} blocks warm={warm}: {n} super-rounds on CTA thread 0s, sweeps {r
 for i, nm in enumerate(names):
     print(f"  {nm:12s} {buf[i] / n:8.0f} cycles/super-round ({100 * buf[i] / tot:.1f}%)")
 print(f"  total        {tot / n:8.0f}")
-sub = ["gram ring wait", "gram staging", "gram fence", "gram syncthreads", "gram issue(t0)", "gram final waits"]
-for i, nm in enumerate(sub):
-    print(f"    {nm:18s} {buf[10 + i] / n:8.0f}")
+nm = max(buf[13], 1)
+print(f"  per matrix: load {buf[10] / nm:.0f}, verdicts {buf[11] / nm:.0f}, epilogue {buf[12] / nm:.0f} cycles "
+      f"({n / nm:.1f} super-rounds per matrix -> {(buf[10] + buf[11] + buf[12]) / n:.0f} per super-round)")
