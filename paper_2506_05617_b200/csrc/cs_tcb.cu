@@ -405,11 +405,16 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         int info = -1;
         bool wait_x = false, wait_v = false;  // incoming panel (in flight into slot a or b)
         int src_pending = 0;
-        auto finish_v = [&]() {  // the incoming V rows have landed: acknowledge the sender's mailbox
+        auto finish_v = [&]() {  // the incoming V rows have landed
             if (wait_v) {
                 mbar_wait(&bar[3], phv);
                 phv ^= 1;
                 wait_v = false;
+                // the mailbox is consumed: drop its dirty L2 lines instead of letting
+                // them be written back to HBM (one 128-byte line per thread)
+                static_assert(SLOT == NT * 128, "one mailbox line per thread");
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(box(src_pending, epoch) + (size_t)tid * 128)
+                             : "memory");
             }
         };
         for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
