@@ -570,6 +570,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 TCB_MARK(2);
                 if (any_rot && !bad) {
                     rot = true;
+#ifdef CS_TCB_CLOCKS
+                    if (tid == 0) atomicAdd(&g_tcb_cycles[any_big ? 15 : 14], 1ull);
+#endif
                     if (!any_big) {
                         // ---- (4a) small angles (every |gamma| / sqrt(alpha beta) <=
                         // GCHECK_TAU): D = Q - I for Q = the product of the rounds'

@@ -26,3 +26,4 @@ print(f"  total        {tot / n:8.0f}")
 nm = max(buf[13], 1)
 print(f"  per matrix: load {buf[10] / nm:.0f}, verdicts {buf[11] / nm:.0f}, epilogue {buf[12] / nm:.0f} cycles "
       f"({n / nm:.1f} super-rounds per matrix -> {(buf[10] + buf[11] + buf[12]) / n:.0f} per super-round)")
+print(f"  rotating super-rounds: {buf[14] / n:.3f} product form, {buf[15] / n:.3f} exp form")
