@@ -41,6 +41,30 @@ static int num_sms() {
     return sms;
 }
 
+// Run-time switches, all read here.  CS_GRAM_CHECK and
+// CS_TCB select documented alternative paths that the tests compare with the
+// default; the planner hooks (cluster size, generic kernel, the slower
+// Gram-blocked / split-role variants) exist only in CS_EXPERIMENTS builds
+// (tools/ab_build.sh).
+struct Knobs {
+    int gram_check = 1;  // CS_GRAM_CHECK: 0 = rotation-free final sweep, 2 = timing experiment
+    bool tcb = true;     // CS_TCB=0: scalar panel kernel for warm-started 256 x 256 + V solves
+    int panel_c = 0, generic_c = 0;  // experiments: force the panel cluster size / the generic kernel
+    bool gram = false, split = false;  // experiments: opt-in panel variants
+};
+static Knobs knobs() {
+    Knobs k;
+    if (const char *e = std::getenv("CS_GRAM_CHECK")) k.gram_check = e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
+    if (const char *e = std::getenv("CS_TCB")) k.tcb = e[0] != '0';
+#ifdef CS_EXPERIMENTS
+    if (const char *e = std::getenv("CS_PANEL_C")) k.panel_c = std::atoi(e);
+    if (const char *e = std::getenv("CS_GENERIC_C")) k.generic_c = std::atoi(e);
+    if (const char *e = std::getenv("CS_GRAM")) k.gram = e[0] == '1';
+    k.split = std::getenv("CS_SPLIT") != nullptr;
+#endif
+    return k;
+}
+
 static void base_shape(int co, int ci, bool wantv, int C, JacShape &s) {
     s = JacShape{};
     const bool wide = co < ci;
@@ -111,7 +135,7 @@ static bool plan_fast(int co, int ci, bool wantv, int C, JacShape &s) {
 // of [X; V] per CTA; a-panel rows in registers, b panel (x2 when C > 1 for
 // the cluster rotation) + a staging copy of the a panel in shared memory.
 template <typename T>
-static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
+static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s, const Knobs &kn) {
     base_shape(co, ci, wantv, C, s);
     s.kind = 2;
     s.ncp = ((s.nc + 4 * C - 1) / (4 * C)) * (4 * C);
@@ -133,7 +157,7 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     // with vectors, X and V rows go to separate warps when 2x the threads fit
     // (each thread then holds only one role's rows: budget/2 per role at 64 regs)
     s.split = (wantv && sizeof(T) == 4 && rplv == rplx && 2 * w * G <= 1024 && w * G % 32 == 0 &&
-               rplx <= budget / 2 && std::getenv("CS_SPLIT") != nullptr) ? 1 : 0;  // opt-in: spills at 64 regs
+               rplx <= budget / 2 && kn.split) ? 1 : 0;  // opt-in: spills at 64 regs
     if (!s.split && rplx + rplv > budget) return false;
     s.G = G;
     s.RPL = rplx;
@@ -149,8 +173,7 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     s.off_send = off;  // staging for the cluster norm gather; Gram mode: G and D
     // Gram-blocked cross phase (opt-in CS_GRAM=1: correct, but 2.8x slower than the
     // scalar cross rounds on cfg5 in SIMT; kept as the skeleton for a tensor-core version)
-    const char *genv = std::getenv("CS_GRAM");
-    s.gram = (sizeof(T) == 4 && w == 16 && !s.split && genv != nullptr && genv[0] == '1' &&
+    s.gram = (sizeof(T) == 4 && w == 16 && !s.split && kn.gram &&
               w * (s.mr + s.Rv) <= 16 * s.threads) ? 1 : 0;  // a-panel staging: 16 per thread
     const size_t gbytes = s.gram ? 2 * (size_t)(2 * w) * (2 * w + 1) * 2 * sizeof(T) : 0;
     off = align16(off + std::max(s.ncp * sizeof(T), gbytes));
@@ -166,9 +189,8 @@ static bool plan_panel(int co, int ci, bool wantv, int C, JacShape &s) {
     s.smem = off;
     s.smem_resident = 1;
     s.nbuf = 1;
-    const char *gc = std::getenv("CS_GRAM_CHECK");  // default on; "0" = rotation-free sweep
     // "2" (timing experiment): check after every rotating sweep, ignore the verdict
-    s.gcheck = (!s.split && !s.gram && !(gc && gc[0] == '0')) ? ((gc && gc[0] == '2') ? 2 : 1) : 0;
+    s.gcheck = (!s.split && !s.gram) ? kn.gram_check : 0;
     return s.smem <= JAC_SMEM_LIMIT;
 }
 
@@ -216,26 +238,26 @@ static bool plan_generic(int co, int ci, bool wantv, int C, bool smem_resident, 
 template <typename T>
 static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
     const int Cs[5] = {1, 2, 4, 8, 16};
-    if (const char *fc = std::getenv("CS_PANEL_C")) {  // experiment hook: force the cluster size
-        if (plan_panel<T>(co, ci, wantv, std::atoi(fc), s)) return true;
+    const Knobs kn = knobs();
+    if (kn.panel_c) {  // experiment hook: force the cluster size
+        if (plan_panel<T>(co, ci, wantv, kn.panel_c, s, kn)) return true;
     }
-    if (const char *fg = std::getenv("CS_GENERIC_C")) {  // experiment hook: generic kernel, cluster C
-        const int c = std::atoi(fg);
-        if (plan_generic<T>(co, ci, wantv, c, true, s)) return true;
-        if (plan_generic<T>(co, ci, wantv, c, false, s)) return true;
+    if (kn.generic_c) {  // experiment hook: generic kernel, cluster C
+        if (plan_generic<T>(co, ci, wantv, kn.generic_c, true, s)) return true;
+        if (plan_generic<T>(co, ci, wantv, kn.generic_c, false, s)) return true;
     }
     for (int i = 0; i < 5; ++i) {
-        if (!plan_panel<T>(co, ci, wantv, Cs[i], s)) continue;
+        if (!plan_panel<T>(co, ci, wantv, Cs[i], s, kn)) continue;
         // small batches: spread each matrix over more CTAs while fewer than
         // 4 CTAs per SM would be queued (cfg4's 394 128^2 blocks: C = 1 19.0 ms,
         // C = 2 12.0 ms, C = 4 13.4 ms; with a 2-per-SM cut they stayed at C = 1)
         int j = i;
         while (j < 4 && count * Cs[j] < 4LL * num_sms()) {
             JacShape t;  // panels narrower than 8 columns only add exchanges (cfg1 16^2)
-            if (!plan_panel<T>(co, ci, wantv, Cs[j + 1], t) || t.P < 8) break;
+            if (!plan_panel<T>(co, ci, wantv, Cs[j + 1], t, kn) || t.P < 8) break;
             ++j;
         }
-        return plan_panel<T>(co, ci, wantv, Cs[j], s);
+        return plan_panel<T>(co, ci, wantv, Cs[j], s, kn);
     }
     for (int i = 0; i < 5; ++i) {
         if (!plan_fast<T>(co, ci, wantv, Cs[i], s)) continue;
@@ -258,14 +280,7 @@ static bool plan(int co, int ci, bool wantv, long long count, JacShape &s) {
 bool tcb_supported(int mr, int nc, bool wantv);
 size_t tcb_workspace(int mr, int nc, bool wantv);
 int tcb_dispatch(const JacArgs<float> &a, void *ws, size_t ws_bytes, cudaStream_t st);
-// experiment switch, read once: CS_TCB=0 keeps the scalar panel kernel
-static bool tcb_enabled() {
-    static const bool on = [] {
-        const char *e = std::getenv("CS_TCB");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
+static bool tcb_enabled() { return knobs().tcb; }
 
 template <typename T>
 static int dispatch(const JacArgs<T> &a, bool wantv, cudaStream_t st, bool dry, long long *ncl) {

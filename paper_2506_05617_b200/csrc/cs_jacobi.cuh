@@ -158,11 +158,44 @@ template <typename T> struct Rot { T cm1, wr, wi; };
 #endif
 constexpr double GCHECK_TAU2 = CS_GCHECK_TAU * CS_GCHECK_TAU;
 
+// Gram-check form of the skip test (the pair is not rotated there): the same
+// rescaling when alpha*beta or |gamma|^2 leaves the normal range
+template <typename T>
+__device__ __forceinline__ bool below_tol(T q, T gr, T gi, T al, T be, T tol) {
+    if (!(q <= (T)1e30 && al * be <= (T)1e30 && al * be >= (T)1e-30 && (q == (T)0 || q >= (T)1e-30 * tol * tol))) {
+        const T inv = (T)1 / (al > be ? al : be);
+        al *= inv; be *= inv; gr *= inv; gi *= inv;
+        q = gr * gr + gi * gi;
+    }
+    return q <= tol * tol * (al * be);
+}
+
+// Column norms beyond ~1e9 / below ~1e-9 (fp32) put alpha*beta and |gamma|^2
+// outside the normal range: the squared skip test would pass every pair
+// (overflow) and the parameter math would turn inf/NaN.  Every
+// quantity below depends only on ratios, so such pairs are rescaled by
+// max(alpha, beta) first (|gamma|^2 <= alpha beta keeps them in range).
+template <typename T>
+__device__ __forceinline__ bool out_of_range(T q, T ab, T tol) {
+    return !(q <= (T)1e30 && ab <= (T)1e30 && ab >= (T)1e-30 && (q == (T)0 || q >= (T)1e-30 * tol * tol));
+}
+template <typename T> __device__ __forceinline__ T recip(T s) { return (T)1 / s; }
+template <> __device__ __forceinline__ float recip<float>(float s) { return __frcp_rn(s); }  // no div subroutine
+template <typename T>
+__device__ __forceinline__ void rescale_pair(T &al, T &be, T &gr, T &gi) {
+    const T inv = recip<T>(al > be ? al : be);
+    al *= inv; be *= inv; gr *= inv; gi *= inv;
+}
+
 template <typename T>
 __device__ __forceinline__ int rot_params(T al, T be, T gr, T gi, T tol, Rot<T> &R) {
     if (!(dfinite(al) && dfinite(be) && dfinite(gr) && dfinite(gi))) return -1;
     if (al == (T)0 || be == (T)0) return 0;
-    const T q = gr * gr + gi * gi;
+    T q = gr * gr + gi * gi;
+    if (out_of_range<T>(q, al * be, tol)) {
+        rescale_pair<T>(al, be, gr, gi);
+        q = gr * gr + gi * gi;
+    }
     if (q <= tol * tol * (al * be)) return 0;
     const T ag = dsqrt(q);
     const T d = be - al, g = (T)2 * ag;
@@ -190,7 +223,11 @@ __device__ __forceinline__ int rot_params<float>(float al, float be, float gr, f
                                                  Rot<float> &R) {
     if (!(isfinite(al) && isfinite(be) && isfinite(gr) && isfinite(gi))) return -1;
     if (al == 0.f || be == 0.f) return 0;
-    const float q = gr * gr + gi * gi;
+    float q = gr * gr + gi * gi;
+    if (out_of_range<float>(q, al * be, tol)) {
+        rescale_pair<float>(al, be, gr, gi);
+        q = gr * gr + gi * gi;
+    }
     if (q <= tol * tol * (al * be)) return 0;
     const float inv_ag = nr_rsqrt(q);
     const float ag = q * inv_ag;

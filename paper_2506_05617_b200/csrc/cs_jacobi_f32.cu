@@ -32,9 +32,11 @@ static int panel_rpl(const JacArgs<float> &a, bool wantv, cudaStream_t st, bool 
     if constexpr (RPL_ >= 4 && RPL_ + RPL_ / 2 <= 16)
         if (wantv && !a.s.split && RPL_ / 2 >= 2 && (a.s.Rv + a.s.G - 1) / a.s.G <= RPL_ / 2)
             return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_ / 2, false>, a, st, dry, ncl);
+#ifdef CS_EXPERIMENTS
     if constexpr (2 * RPL_ <= 16 && true)
         if (wantv && a.s.split)
             return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_, true>, a, st, dry, ncl);
+#endif
     if constexpr (2 * RPL_ <= 16)
         if (wantv) return launch_cluster_kernel<float, C_>(jacobi_panel_kernel<float, C_, RPL_, RPL_, false>, a, st, dry, ncl);
     if constexpr (RPL_ <= 16)

@@ -997,7 +997,7 @@ __device__ __forceinline__ void gram_block(const cplx_t<T> *X, int ldx, int px,
                 const T q = v[0] * v[0] + other * other;
                 const T ai = nrm[gi], aj = nrm[gj];
                 if (!(isfinite(q) && isfinite(ai) && isfinite(aj))) bad = true;
-                else if (ai != (T)0 && aj != (T)0 && q > tol * tol * (ai * aj)) bad = true;
+                else if (ai != (T)0 && aj != (T)0 && !below_tol<T>(q, v[0], other, ai, aj, tol)) bad = true;
             }
         }
         // reconverge before the next task's shuffles: a warp left diverged here
@@ -1197,13 +1197,16 @@ jacobi_panel_kernel(const JacArgs<T> a) {
             if (tid < 32) start_pos[tid] = pos[tid];
 
             int fl;
+#ifdef CS_EXPERIMENTS  // slower opt-in variants: experiment builds only
             if constexpr (SPLIT) {
                 fl = panel_within_split<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
                 fl |= panel_cross_split<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
             } else if (s.gram) {
                 fl = panel_within<T, C, RPLX, RPLV>(s, smem, Abuf, Bbuf, start_a, start_b, tol);
                 fl |= panel_cross_gram<T, C, RPLX, RPLV>(s, smem, rank, Abuf, Bbuf0, tol);
-            } else {
+            } else
+#endif
+            {
 #ifdef CS_PHASE_CLOCKS
                 long long c0 = clock64();
 #endif

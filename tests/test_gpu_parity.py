@@ -7,6 +7,8 @@ fp64; the reference's own unit-test tolerances where those are tighter
 (pkg/tests/test_symbol.py, test_blocksvd.py, test_acceptance.py).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -351,7 +353,11 @@ def test_materialize_orthonormal_and_range(cuda):
                                               ("CS_SPLIT", (64, 64), 320)])
 def test_opt_in_kernel_variants_match_oracle(cuda, orc, monkeypatch, flag, shape, count):
     """The opt-in Gram-blocked and split-role panel variants (DESIGN.md 3);
-    batch sizes keep the planner on the panel widths those variants need."""
+    batch sizes keep the planner on the panel widths those variants need.
+    They are compiled only into experiment builds (tools/ab_build.sh with
+    CS_AB_FLAGS=-DCS_EXPERIMENTS, selected by CS_LIBPATH)."""
+    if "CS_LIBPATH" not in os.environ:
+        pytest.skip("opt-in panel variants exist only in CS_EXPERIMENTS builds")
     co, ci = shape
     rng = np.random.default_rng(co + ci)
     A = (rng.standard_normal((count, co, ci)) + 1j * rng.standard_normal((count, co, ci))) / np.sqrt(ci)
@@ -460,3 +466,18 @@ def test_fp64_cfg5_shape_panel_path(cuda, orc):
         assert np.abs((U[f] * s[f]) @ V[f].conj().T - A[f]).max() <= 1e-10 * s[f][0]
         assert np.abs(U[f].conj().T @ U[f] - np.eye(ci)).max() <= 1e-9
         assert np.abs(V[f].conj().T @ V[f] - np.eye(ci)).max() <= 1e-9
+
+
+@pytest.mark.parametrize("scale", [1e12, 1e-12])
+def test_extreme_column_norms_fp32(cuda, orc, scale):
+    """fp32 column norms whose product alpha*beta leaves the float range
+    (ADVICE r01): the skip test must not pass every pair (overflow) or
+    rotate denormal noise (underflow); sigma scales exactly with the block."""
+    rng = np.random.default_rng(7)
+    A = (rng.standard_normal((4, 32, 32)) + 1j * rng.standard_normal((4, 32, 32))) / np.sqrt(32)
+    ref, _ = orc.svd_values(A)
+    blocks = torch.from_numpy((A * scale).astype(np.complex64)).to(cuda)
+    out = engine.batched_svd(blocks, "f32", False)
+    assert (out.info.cpu().numpy() > 0).all()
+    sig = out.sigma.cpu().numpy().astype(np.float64) / scale
+    assert per_freq_rel_err(sig, ref).max() <= TOL32
