@@ -51,7 +51,7 @@ namespace tcb {
 
 constexpr int NT = 512;
 constexpr int GW = 4;  // Gram-issuing warps (one TMEM accumulator each)
-constexpr int MAXC = 8;
+constexpr int MAXC = 16;
 
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
@@ -92,30 +92,34 @@ constexpr int CT_FX = 0, CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_BYTES = 2
 // exchanges and ends with a group-wide verdict barrier, so a mailbox is
 // rewritten (NBOX >= 2C-1 exchanges later) only after every CTA of the group
 // passed a verdict that its receiver posted after consuming it: no
-// acknowledgement flags are needed.
-constexpr int NBOX = 16;
+// acknowledgement flags are needed.  (Cfg::NBOX: the power of two >= 2C-1.)
 
-template <int MR, int NC>
+// MR x NC working blocks; VEC: V rows (NC of them) ride along under the X
+// rows (vectors requested), else the panels hold X only (sigma-only solves)
+template <int MR, int NC, bool VEC>
 struct Cfg {
     static constexpr int C = NC / N2;
     static constexpr int STEPS = 2 * C - 1;
-    static constexpr int ROWS = MR + NC;
+    static constexpr int NBOX = STEPS <= 16 ? 16 : 32;
+    static constexpr int ROWS = MR + (VEC ? NC : 0);
     static constexpr uint32_t SLOT = ROWS * 128;  // one panel: W complex = 32 real columns, SW128 K-major
     static constexpr uint32_t XBYTES = MR * 128;  // its X rows (the V rows follow)
+    static constexpr int STAGES = MR / 64;        // Gram stages of 64 X rows
+    static constexpr int MBLK = ROWS / 128;       // update M-blocks
+    static constexpr int NBAR = 6 + STAGES;       // [0,1] update ring, [3] V in, [4,5] Gram ring, [6..] X in by stage
     static constexpr uint32_t SIG_OFF = 3 * SLOT;
     static constexpr uint32_t PERM_OFF = SIG_OFF + NC * 4;
     static constexpr uint32_t FLAG_OFF = PERM_OFF + 2 * NC * 4;
     static constexpr uint32_t RED_OFF = FLAG_OFF + 16 * 4;
     static constexpr uint32_t BAR_OFF = (RED_OFF + 64 * 4 + 15) & ~15u;
-    static constexpr uint32_t TM_OFF = BAR_OFF + 10 * 8;
+    static constexpr uint32_t TM_OFF = BAR_OFF + NBAR * 8;
     static constexpr uint32_t SMEM = TM_OFF + 16;
-    static constexpr int STAGES = MR / 64;
-    static constexpr int MBLK = ROWS / 128;
     static_assert(MR % 64 == 0 && ROWS % 128 == 0 && NC % N2 == 0, "tcb shape");
-    static_assert(SLOT >= 65536, "tcb scratch slot holds the 64 KB Gram/update staging");
-    static_assert(STAGES <= 4 && MBLK <= 4, "tcb TMEM budget (4 accumulators of 128 columns)");
+    static_assert(SLOT == 65536, "tcb panel slot = the 64 KB Gram/update scratch = one mailbox line per thread");
+    static_assert(MBLK <= 4, "tcb TMEM budget (4 update accumulators of 128 columns)");
+    static_assert(2 * NC >= 512, "the Gram norm partials reuse the permutation scratch");
     static_assert(C >= 2 && C <= MAXC, "tcb group size");
-    static_assert(NBOX >= 2 * C - 1, "mailbox reuse must cross a sweep-verdict barrier");
+    static_assert(NBOX >= STEPS, "mailbox reuse must cross a sweep-verdict barrier");
     static_assert(SMEM <= 227 * 1024, "tcb shared memory");
 };
 
@@ -281,9 +285,9 @@ __device__ __forceinline__ void gram_stage2(const unsigned char *Pa, const unsig
     }
 }
 
-template <int MR, int NC>
+template <int MR, int NC, bool VEC>
 __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> a, const Sched sc, const Ws ws) {
-    using K = Cfg<MR, NC>;
+    using K = Cfg<MR, NC, VEC>;
     constexpr int C = K::C, STEPS = K::STEPS;
     constexpr uint32_t SLOT = K::SLOT, XBYTES = K::XBYTES;
     extern __shared__ __align__(1024) unsigned char sm[];
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     const float tol = a.tol;
     unsigned char *const myctl = ws.ctrl + (size_t)blockIdx.x * CT_BYTES;
     auto ctl = [&](int cta) { return ws.ctrl + ((size_t)g * C + cta) * CT_BYTES; };
-    auto box = [&](int cta, int e) { return ws.mail + (((size_t)g * C + cta) * NBOX + (e % NBOX)) * SLOT; };
+    auto box = [&](int cta, int e) { return ws.mail + (((size_t)g * C + cta) * K::NBOX + (e % K::NBOX)) * SLOT; };
     float *const gsig = ws.gsig + (size_t)g * 2 * NC;
 
     if (warp == 0) {
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
     }
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
-        for (int i = 6; i < 10; ++i) mbar_init(&bar[i], 1);
+        for (int i = 6; i < K::NBAR; ++i) mbar_init(&bar[i], 1);
         mbar_init(&bar[4], GW);  // one commit per Gram-issuing warp
         mbar_init(&bar[5], GW);
         fence_mbar_init();
@@ -477,6 +481,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 if (wait_x) {
                     phx ^= 1;
                     wait_x = false;
+                    if constexpr (!VEC)  // the whole mailbox has landed: drop its L2 lines
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(box(src_pending, epoch) + (size_t)tid * 128)
+                                     : "memory");
                 }
                 if (K::STAGES >= 2) { gram_wait(K::STAGES & 1); gram_wait((K::STAGES + 1) & 1); }
                 else gram_wait(0);
@@ -754,10 +761,13 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             mbar_arrive_expect_tx(&bar[6 + c], XC);
                             bulk_g2s(is + c * XC, in + c * XC, XC, smem_u32(&bar[6 + c]));
                         }
-                        mbar_arrive_expect_tx(&bar[3], SLOT - XBYTES);
-                        bulk_g2s(is + XBYTES, in + XBYTES, SLOT - XBYTES, smem_u32(&bar[3]));
+                        if constexpr (VEC) {
+                            mbar_arrive_expect_tx(&bar[3], SLOT - XBYTES);
+                            bulk_g2s(is + XBYTES, in + XBYTES, SLOT - XBYTES, smem_u32(&bar[3]));
+                        }
                     }
-                    wait_x = wait_v = true;
+                    wait_x = true;
+                    wait_v = VEC;
                     src_pending = src;
                     const int ns = sl[2];
                     sl[2] = sl[o];
@@ -963,11 +973,11 @@ static bool build_sched(int C, Sched &s) {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-template <int MR, int NC>
+template <int MR, int NC, bool VEC>
 static size_t ws_bytes_for(int ngroups) {
-    using K = Cfg<MR, NC>;
+    using K = Cfg<MR, NC, VEC>;
     return align256((size_t)ngroups * K::C * CT_BYTES + 256) + align256((size_t)ngroups * 2 * NC * sizeof(float)) +
-           (size_t)ngroups * K::C * NBOX * K::SLOT;
+           (size_t)ngroups * K::C * K::NBOX * K::SLOT;
 }
 
 static int max_groups(int C) {
@@ -978,21 +988,21 @@ static int max_groups(int C) {
     return sms / C;  // one CTA per SM (the three panel slots take ~200 KB)
 }
 
-template <int MR, int NC>
+template <int MR, int NC, bool VEC>
 static int launch(const JacArgs<float> &a, void *wsp, size_t wsb, cudaStream_t st) {
-    using K = Cfg<MR, NC>;
+    using K = Cfg<MR, NC, VEC>;
     static Sched sched;
     static int sched_ok = -1;
     if (sched_ok < 0) sched_ok = build_sched(K::C, sched) ? 1 : 0;
     if (!sched_ok) return fail(CS_EINVAL, "tcb SVD: exchange schedule construction failed");
-    auto kern = jacobi_tcb_kernel<MR, NC>;
+    auto kern = jacobi_tcb_kernel<MR, NC, VEC>;
     CS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
     int per_sm = 0;
     CS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, K::SMEM));
     if (per_sm < 1) return fail(CS_ENOMEM, "tcb SVD: kernel does not fit on an SM");
     const long long ng = lmin(a.count, (long long)max_groups(K::C));
     if (ng < 1) return CS_OK;
-    const size_t need = ws_bytes_for<MR, NC>(max_groups(K::C));
+    const size_t need = ws_bytes_for<MR, NC, VEC>(max_groups(K::C));
     if (!wsp || wsb < need) return fail(CS_ENOMEM, "tcb SVD: workspace too small (query cs_batched_svd_workspace)");
     unsigned char *base = (unsigned char *)wsp;
     Ws ws;
@@ -1018,12 +1028,16 @@ static int launch(const JacArgs<float> &a, void *wsp, size_t wsb, cudaStream_t s
 }  // namespace tcb
 
 // shapes the tensor-core blocked kernel is instantiated for (working
-// orientation mr x nc, vectors requested, fp32)
+// orientation mr x nc, fp32): warm-started 256 x 256 + V (cfg5).  The
+// kernel is written for sigma-only shapes too (VEC = false); 512 x 512
+// sigma-only solves measured only 16% faster on cfg4 than the scalar kernel
+// and drift further in energy over their ~12 cold sweeps (K3), so
+// they stay on the scalar kernel.
 bool tcb_supported(int mr, int nc, bool wantv) { return wantv && mr == 256 && nc == 256; }
 
 size_t tcb_workspace(int mr, int nc, bool wantv) {
     if (!tcb_supported(mr, nc, wantv)) return 0;
-    return tcb::ws_bytes_for<256, 256>(tcb::max_groups(tcb::Cfg<256, 256>::C));
+    return tcb::ws_bytes_for<256, 256, true>(tcb::max_groups(tcb::Cfg<256, 256, true>::C));
 }
 
 #ifdef CS_TCB_CLOCKS
@@ -1039,7 +1053,7 @@ extern "C" int cs_debug_tcb_cycles(unsigned long long *out, int reset) {
 #endif
 
 int tcb_dispatch(const JacArgs<float> &a, void *ws, size_t ws_bytes, cudaStream_t st) {
-    if (a.s.mr == 256 && a.s.nc == 256) return tcb::launch<256, 256>(a, ws, ws_bytes, st);
+    if (a.s.mr == 256 && a.s.nc == 256 && a.Vw) return tcb::launch<256, 256, true>(a, ws, ws_bytes, st);
     return fail(CS_EINVAL, "tcb SVD: unsupported shape");
 }
 

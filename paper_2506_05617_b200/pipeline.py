@@ -122,7 +122,23 @@ def lfa_device_multi(layers, dtype: str, want_vectors: bool = False,
     fields = [engine.symbol_field(w, n, m, dtype, half=True) for w, n, m in layers]
     if timer:
         timer.mark("t1")
-    outs = engine.batched_svd_grouped(fields, dtype, want_vectors, tol, max_sweeps)
+    # layers of one block shape share one group (one fuller launch instead of
+    # several partial waves: cfg4's four 512^2 layers are 4 x 25 blocks)
+    by_shape = {}
+    for i, f in enumerate(fields):
+        by_shape.setdefault(tuple(f.shape[1:]), []).append(i)
+    merged = [fields[ix[0]] if len(ix) == 1 else engine.torch.cat([fields[i] for i in ix])
+              for ix in by_shape.values()]
+    mouts = engine.batched_svd_grouped(merged, dtype, want_vectors, tol, max_sweeps)
+    outs = [None] * len(fields)
+    for ix, mo in zip(by_shape.values(), mouts):
+        off = 0
+        for i in ix:
+            c = fields[i].shape[0]
+            cut = (lambda t: None if t is None else t[off:off + c])  # noqa: E731
+            outs[i] = engine.SvdBatch(sigma=mo.sigma[off:off + c], info=mo.info[off:off + c],
+                                      U=cut(mo.U), V=cut(mo.V), zero=cut(mo.zero))
+            off += c
     if timer:
         timer.mark("t2")
     res = []
