@@ -363,10 +363,15 @@ def run_ours(args, wl, rank, world, local_rank):
         outs = []
         for i, (l, w) in enumerate(zip(layers, w_dev)):
             tm = timers[i] if timers else None
+            # the solve compute_spectrum runs: values-only calls run the vectors
+            # solve (factors dropped) whenever that is the panel/tensor-core kernel,
+            # so values_only True/False agree bitwise (CS/pipeline.py:40-42)
+            vec = wl.vectors or engine.values_via_vectors(engine.half_grid_count(l.n, l.m),
+                                                         l.c_out, l.c_in, dt)
             if world > 1:
-                outs.append(lfa_sharded(w, l.n, l.m, dt, wl.vectors, timer=tm))
+                outs.append(lfa_sharded(w, l.n, l.m, dt, vec, timer=tm))
             else:
-                outs.append(cs.lfa_device(w, l.n, l.m, dt, wl.vectors, timer=tm))
+                outs.append(cs.lfa_device(w, l.n, l.m, dt, vec, timer=tm))
         return outs
 
     def barrier():
@@ -435,17 +440,19 @@ def run_ours(args, wl, rank, world, local_rank):
                                     if wl.vectors else
                                     "Golub-Reinsch sigma-only count x4 complex per unique block (SURVEY 8(d))")}
         # DRAM traffic per step from the committed ncu capture of this workload
-        # (profiles/r01k_traffic_cfg5.json; null for other workloads / N > 1)
+        # (profiles/r02_traffic_cfg5.json; null for other workloads / N > 1):
+        # the SVD phase = warm-start GEMMs + K3 + the seeds' K2 launch
         trf = {}
-        tpath = os.path.join(ROOT, "profiles", "r01k_traffic_cfg5.json")
+        tpath = os.path.join(ROOT, "profiles", "r02_traffic_cfg5.json")
         if world == 1 and os.path.exists(tpath):
             tj = json.load(open(tpath))
             if tj.get("workload") == workload_config(wl, world).get("workload"):
                 trf = tj["per_step"]
-        if "jacobi_panel_kernel" in trf:
-            j = trf["jacobi_panel_kernel"]
-            roofline["traffic"] = (j["dram_read_GB"] + j["dram_write_GB"]) * 1e9
-            roofline["traffic_source"] = "ncu dram__bytes_read+write per step, profiles/r01k_traffic_cfg5.json"
+        svd_k = [k for k in ("jacobi_tcb_kernel", "warm_gemm_tc_kernel", "jacobi_panel_kernel") if k in trf]
+        if svd_k:
+            roofline["traffic"] = sum((trf[k]["dram_read_GB"] + trf[k]["dram_write_GB"]) * 1e9 for k in svd_k)
+            roofline["traffic_source"] = ("ncu dram__bytes_read+write per step of " + " + ".join(svd_k) +
+                                          ", profiles/r02_traffic_cfg5.json")
         asm_b = sum(asm_bytes(l, c) for l, c in zip(layers, shares))
         hbm = peaks.get("hbm_gbs", 6650.0)
         k1_s = sum(k1) / args.steps

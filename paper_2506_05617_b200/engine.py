@@ -540,10 +540,13 @@ def batched_svd_warm(blocks, dtype: str, n: int, m: int, u0: int, tol=DEFAULT_SV
 
 def use_warm_start(count: int, co: int, ci: int, dtype: str, want_vectors: bool,
                    requested=None) -> bool:
-    """Warm start pays off when vectors are computed anyway (seeds need V)."""
+    """Warm start pays off when vectors are computed anyway (seeds need V)
+    and the blocks are not tiny: 16 x 16 blocks converge cold in ~7 cheap
+    sweeps, and the staged warm launches cost more than they save (cfg1:
+    3.3 ms per call warm vs ~1 ms cold).  CS_WARM_START=0/1 forces it."""
     env = os.environ.get("CS_WARM_START")
     if requested is None:
-        requested = (env != "0") if env is not None else want_vectors
+        requested = (env != "0") if env is not None else (want_vectors and min(co, ci) >= 32)
     if not requested or count < 3:
         return False
     return plan_kind(count, co, ci, dtype, True) == 2
