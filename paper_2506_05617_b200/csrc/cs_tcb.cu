@@ -56,7 +56,7 @@ constexpr int MAXC = 16;
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
-__device__ unsigned long long g_tcb_cycles[16];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
+__device__ unsigned long long g_tcb_cycles[24];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
         if (tid == 0) {                                                              \
@@ -178,25 +178,44 @@ __device__ __forceinline__ unsigned spin_tag(const void *p, unsigned tag, int wh
     return v;
 }
 
-// C = s * A B (+ I) on 32 x 32 complex matrices in shared memory (stride LDG)
+// C = s * A B (+ I) on 32 x 32 complex matrices in shared memory (stride LDG).
+// Register-blocked: each of the first 256 threads owns rows (i, i+16) x
+// columns (j, j+16), so every shared-memory load feeds two complex MACs (the
+// one-output-pair-per-thread form was shared-memory bound: 23.8k cycles per
+// exp(E) with ~14 of these products).  C must not alias A or B.
 __device__ __forceinline__ void cgemm32(const float2 *A, const float2 *B, float2 *Cm, float s, bool addI) {
-    const int t = threadIdx.x, i = t >> 4, j = t & 15;
-    float2 c0 = make_float2(0.f, 0.f), c1 = c0;
-#pragma unroll 8
+    const int t = threadIdx.x;
+    if (t >= 256) return;
+    const int i = t >> 4, j = t & 15;
+    float2 c[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) c[u][v] = make_float2(0.f, 0.f);
+#pragma unroll 4
     for (int k = 0; k < N2; ++k) {
-        const float2 a = A[i * LDG + k], b0 = B[k * LDG + j], b1 = B[k * LDG + j + 16];
-        c0.x = fmaf(a.x, b0.x, fmaf(-a.y, b0.y, c0.x));
-        c0.y = fmaf(a.x, b0.y, fmaf(a.y, b0.x, c0.y));
-        c1.x = fmaf(a.x, b1.x, fmaf(-a.y, b1.y, c1.x));
-        c1.y = fmaf(a.x, b1.y, fmaf(a.y, b1.x, c1.y));
+        float2 a[2], bb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            a[u] = A[(i + 16 * u) * LDG + k];
+            bb[u] = B[k * LDG + j + 16 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                c[u][v].x = fmaf(a[u].x, bb[v].x, fmaf(-a[u].y, bb[v].y, c[u][v].x));
+                c[u][v].y = fmaf(a[u].x, bb[v].y, fmaf(a[u].y, bb[v].x, c[u][v].y));
+            }
     }
-    c0.x *= s; c0.y *= s; c1.x *= s; c1.y *= s;
-    if (addI) {
-        if (i == j) c0.x += 1.f;
-        if (i == j + 16) c1.x += 1.f;
-    }
-    Cm[i * LDG + j] = c0;
-    Cm[i * LDG + j + 16] = c1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            float2 r = make_float2(c[u][v].x * s, c[u][v].y * s);
+            if (addI && i + 16 * u == j + 16 * v) r.x += 1.f;
+            Cm[(i + 16 * u) * LDG + j + 16 * v] = r;
+        }
 }
 
 // D = exp(E) - I for a skew-Hermitian E (in Em, overwritten by the scaled E;
@@ -650,7 +669,11 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             }
                         }
                         __syncthreads();
+#ifdef CS_TCB_CLOCKS
+                        const long long te = clock64();
+#endif
                         expm_minus_identity(Em, Tm, Dm, red);
+                        TCB_ADD(16, te);
                     }
                     TCB_MARK(3);
                     // ---- (5) B operand (D~, hi | lo) and (6) update P += P D
@@ -1043,9 +1066,9 @@ size_t tcb_workspace(int mr, int nc, bool wantv) {
 #ifdef CS_TCB_CLOCKS
 extern "C" int cs_debug_tcb_cycles(unsigned long long *out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return 4;
-    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 16);
+    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 24);
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[24] = {};
         cudaMemcpyToSymbol(tcb::g_tcb_cycles, z, sizeof(z));
     }
     return 0;
