@@ -50,6 +50,10 @@ namespace cs {
 namespace tcb {
 
 constexpr int NT = 512;
+#ifndef CS_K3_TAU
+#define CS_K3_TAU 0.35f  // measured: 0.05 2901 ms, 0.2 2722, 0.35 2666, 0.5 2689, never-exp 2728 (cfg5 warm SVD)
+#endif
+constexpr float K3_TAU = CS_K3_TAU;  // small-angle (product) vs large-angle (exp) combination
 constexpr int GW = 4;  // Gram-issuing warps (one TMEM accumulator each)
 constexpr int MAXC = 16;
 
@@ -585,7 +589,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     inner_pair(full, tid % W, tid / W, p, qq);
                     const float2 gv = Gm[p * LDG + qq];
                     Rot<float> R;
-                    act = rot_params<float>(Gm[p * LDG + p].x, Gm[qq * LDG + qq].x, gv.x, gv.y, tol, R);
+                    const float al = Gm[p * LDG + p].x, be = Gm[qq * LDG + qq].x;
+                    act = rot_params<float>(al, be, gv.x, gv.y, tol, R);
+                    // "large": |gamma| / sqrt(alpha beta) > K3_TAU selects the exp combination
+                    if (act > 0) act = (gv.x * gv.x + gv.y * gv.y > K3_TAU * K3_TAU * al * be) ? 2 : 1;
                     Prm<float> pm;
                     pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
                     prm[tid] = pm;
