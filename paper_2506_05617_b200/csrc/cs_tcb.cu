@@ -444,7 +444,28 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                              : "memory");
             }
         };
-        for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+        // sweep verdicts (OR over the group, double-buffered by sweep parity) are
+        // posted at the end of a sweep and collected after the first Gram and
+        // angles of the next one: that super-round works on the pairing the
+        // sweep ended on (odd sweeps run backwards) and changes no panel before
+        // the collection, so the wait for the group's slowest CTA overlaps it
+        bool vpend = false, stop = false;
+        auto collect_verdict = [&]() {
+#ifdef CS_TCB_CLOCKS
+            const long long tv = clock64();
+#endif
+            if (tid == 0) {
+                unsigned any = 0;
+                for (int d = 0; d < C; ++d) any |= spin_tag(ctl(d) + CT_VERD + 4 * (vseq & 1), vseq, 4);
+                flags[0] = (int)(any & 3u);
+            }
+            __syncthreads();
+            const int v = flags[0];
+            __syncthreads();
+            TCB_ADD(11, tv);
+            return v;  // bit 0: any rotation, bit 1: non-finite
+        };
+        for (int sweep = 0; sweep < a.max_sweeps && !stop; ++sweep) {
             const bool fwd = (sweep & 1) == 0;
             bool rot = false, bad = false;
 #pragma unroll 1
@@ -601,6 +622,15 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const int any_big = __syncthreads_or(act > 1);
                 if (__syncthreads_or(act < 0)) bad = true;
                 TCB_MARK(2);
+                if (vpend) {  // the previous sweep's verdict, before this sweep changes anything
+                    vpend = false;
+                    const int v = collect_verdict();
+                    if ((v & 2) || !(v & 1)) {
+                        if (!(v & 2)) info = sweep;  // sweep `sweep - 1` (0-based) was rotation-free
+                        stop = true;
+                        break;
+                    }
+                }
                 if (any_rot && !bad) {
                     rot = true;
 #ifdef CS_TCB_CLOCKS
@@ -810,26 +840,16 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 }
                 TCB_MARK(6);
             }
-            // ---- sweep verdict, OR-ed over the group (double-buffered by sweep parity)
-#ifdef CS_TCB_CLOCKS
-            tcb_m = clock64();
-#endif
+            if (stop) break;
+            // ---- post this sweep's verdict; the last allowed sweep collects it here
             ++vseq;
-            if (tid == 0) {
+            if (tid == 0)
                 st_rel(myctl + CT_VERD + 4 * (vseq & 1), (vseq << 2) | (bad ? 2u : 0u) | (rot ? 1u : 0u));
-                unsigned any = 0;
-                for (int d = 0; d < C; ++d) any |= spin_tag(ctl(d) + CT_VERD + 4 * (vseq & 1), vseq, 4);
-                flags[0] = any & 1;
-                flags[1] = (any >> 1) & 1;
-            }
-            __syncthreads();
-            const int any_rot = flags[0], any_bad = flags[1];
-            __syncthreads();
-            TCB_ADD(11, tcb_m);
-            if (any_bad) break;
-            if (!any_rot) {
-                info = sweep + 1;
-                break;
+            vpend = true;
+            if (sweep + 1 == a.max_sweeps) {
+                vpend = false;
+                const int v = collect_verdict();
+                if (!(v & 2) && !(v & 1)) info = sweep + 1;
             }
         }
 
