@@ -448,7 +448,11 @@ extern "C" int cs_batched_svd_grouped(const cs_svd_group *groups, int num_groups
                               max_sweeps, groups[0].sigma,
                               groups[0].U, groups[0].V, groups[0].info, groups[0].zero_sigma,
                               workspace, workspace_bytes, stream);
-    // fork: every group on its own stream so small and large shapes share the SMs
+    // fork: every group on its own stream so small and large shapes share the SMs.
+    // The side streams are created per call: a pool of long-lived streams
+    // reused across calls measured slower on cfg4 (380 vs 340 ms per step,
+    // same box, two runs each) -- plausibly long-lived streams sharing a
+    // hardware work queue with the caller's stream.
     cudaEvent_t fork_ev;
     CS_CUDA_TRY(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     CS_CUDA_TRY(cudaEventRecord(fork_ev, st));
