@@ -91,7 +91,8 @@ struct Ws {
     unsigned char *mail;  // per CTA [NBOX] outgoing panels
     int ngroups;
 };
-constexpr int CT_FX = 0, CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_BYTES = 256;  // VERD/EPI/WORK: [2] by parity
+constexpr int CT_FX = 0, CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_META = 256, CT_BYTES = 512;
+// VERD/EPI/WORK: [2] by parity; META: [16] by exchange (the outgoing panel's modified / tested stamps)
 // mailboxes per CTA: exchange e writes mailbox e % NBOX.  A sweep has 2C-2
 // exchanges and ends with a group-wide verdict barrier, so a mailbox is
 // rewritten (NBOX >= 2C-1 exchanges later) only after every CTA of the group
@@ -431,6 +432,17 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         TCB_ADD(10, tcb_m);
         int info = -1;
         bool wait_x = false, wait_v = false;  // incoming panel (in flight into slot a or b)
+        // Skipping converged pair tests.  A pair block that passed its test at
+        // super-round k and whose panels are unmodified since would pass the
+        // identical (deterministic) test again, so its Gram, read-back and angles
+        // are skipped -- results are bitwise those of testing.  Stamps (super-round
+        // numbers of this matrix, group-uniform): per role the panel's last
+        // modification and last within-panel test (they travel with the panel
+        // through the exchange), per step this CTA's last cross test (CTA c meets
+        // the same panel pair at step t in every sweep).
+        unsigned sr = 0, mod_r[2] = {0u, 0u}, wt_r[2] = {0u, 0u}, ctest[K::STEPS];
+#pragma unroll
+        for (int q = 0; q < K::STEPS; ++q) ctest[q] = 0u;
         int src_pending = 0;
         auto finish_v = [&]() {  // the incoming V rows have landed
             if (wait_v) {
@@ -488,7 +500,24 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;
                 unsigned char *const outbox = box(rank, epoch + 1);
 
+                ++sr;
+                const unsigned mod_max = mod_r[0] > mod_r[1] ? mod_r[0] : mod_r[1];
+                const bool skip = ctest[t] > mod_max && (!full || (wt_r[0] > mod_r[0] && wt_r[1] > mod_r[1]));
+                int any_rot = 0, any_big = 0;
+                Prm<float> *prm = reinterpret_cast<Prm<float> *>(RG + SC_PRM);
+                const int nround = full ? N2 - 1 : W;
                 TCB_MARK(7);
+                if (skip) {  // no test: only the incoming panel's X rows must land
+                    if (wait_x) {
+#pragma unroll 1
+                        for (int st = 0; st < K::STAGES; ++st) mbar_wait(&bar[6 + st], phx);
+                        phx ^= 1;
+                        wait_x = false;
+                        if constexpr (!VEC)
+                            asm volatile("discard.global.L2 [%0], 128;" ::"l"(box(src_pending, epoch) + (size_t)tid * 128)
+                                         : "memory");
+                    }
+                } else {
                 // ---- (1) Gram: STAGES x 64 X rows, transposed hi|lo staging, 2-slot ring.
                 // The 8 K-steps of a stage are issued by GW warps (2 each), warp w
                 // accumulating its K-steps of every stage in accumulator w, so GW
@@ -602,8 +631,6 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 TCB_MARK(1);
                 // ---- (3) every pair's rotation from G at once (the reference's test
                 // and root, rot_params), slot k of round r at prm[16 r + k]
-                Prm<float> *prm = reinterpret_cast<Prm<float> *>(RG + SC_PRM);
-                const int nround = full ? N2 - 1 : W;
                 int act = 0;
                 if (tid < nround * W) {
                     int p, qq;
@@ -618,9 +645,13 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
                     prm[tid] = pm;
                 }
-                const int any_rot = __syncthreads_or(act > 0);
-                const int any_big = __syncthreads_or(act > 1);
+                any_rot = __syncthreads_or(act > 0);
+                any_big = __syncthreads_or(act > 1);
                 if (__syncthreads_or(act < 0)) bad = true;
+                ctest[t] = sr;
+                if (full) wt_r[0] = wt_r[1] = sr;
+                if (any_rot && !bad) mod_r[0] = mod_r[1] = sr;
+                }  // !skip
                 TCB_MARK(2);
                 if (vpend) {  // the previous sweep's verdict, before this sweep changes anything
                     vpend = false;
@@ -810,10 +841,16 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         // thread's mailbox stores (the cooperative-groups grid-sync pattern)
                         __threadfence();
                         fence_proxy_async_global();
+                        unsigned *meta = reinterpret_cast<unsigned *>(myctl + CT_META + 8 * (epoch % 16));
+                        meta[0] = mod_r[o];
+                        meta[1] = wt_r[o];
                         st_rel(myctl + CT_FX, epoch);
                         const unsigned char *in = box(src, epoch);
                         const uint32_t is = smem_u32(sm + sl[2] * SLOT);
                         spin_ge(ctl(src) + CT_FX, epoch, 2);
+                        const unsigned *rm = reinterpret_cast<const unsigned *>(ctl(src) + CT_META + 8 * (epoch % 16));
+                        flags[4] = (int)__ldcg(rm);
+                        flags[5] = (int)__ldcg(rm + 1);
                         fence_proxy_async_global();
                         constexpr uint32_t XC = XBYTES / K::STAGES;  // the X rows of one Gram stage
 #pragma unroll
@@ -835,6 +872,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     ia = sc.ida[t2][rank];
                     ib = sc.idb[t2][rank];
                     __syncthreads();
+                    mod_r[o] = (unsigned)flags[4];  // the incoming panel's stamps
+                    wt_r[o] = (unsigned)flags[5];
                 } else {
                     __syncthreads();
                 }
