@@ -667,6 +667,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #ifdef CS_TCB_CLOCKS
                     if (tid == 0) atomicAdd(&g_tcb_cycles[any_big ? 15 : 14], 1ull);
 #endif
+#ifdef CS_TCB_CLOCKS
+                    const long long tpf = clock64();
+#endif
                     if (!any_big) {
                         // ---- (4a) small angles (every |gamma| / sqrt(alpha beta) <=
                         // GCHECK_TAU): D = Q - I for Q = the product of the rounds'
@@ -679,17 +682,22 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             // its current pair in registers; the b-columns move one lane down
                             // per round (after W rounds every lane holds its own again).
                             float2 x = make_float2(0.f, 0.f), y = x;
-#pragma unroll 1
+#pragma unroll 4
                             for (int r = 0; r < W; ++r) {
                                 const Prm<float> pm = prm[r * W + k];
-                                if (pm.act > 0) {
-                                    const int qq = W + ((k + r) & (W - 1));
-                                    Rot<float> R;
-                                    R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
-                                    rot_apply<float>(x, y, R);
-                                    if (i2 == k) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
-                                    if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
-                                }
+                                // branch-free (the lanes of a half-warp differ in act): rotate
+                                // a copy and select it where the pair is active (a warp-uniform
+                                // skip of rounds without an active pair measured slower)
+                                const int qq = W + ((k + r) & (W - 1));
+                                Rot<float> R;
+                                R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                                float2 xr = x, yr = y;
+                                rot_apply<float>(xr, yr, R);
+                                if (i2 == k) { xr.x += R.cm1; yr.x += R.wr; yr.y += R.wi; }
+                                if (i2 == qq) { xr.x -= R.wr; xr.y += R.wi; yr.x += R.cm1; }
+                                const bool on = pm.act > 0;
+                                x = on ? xr : x;
+                                y = on ? yr : y;
                                 y.x = __shfl_sync(0xffffffffu, y.x, (k + 1) & (W - 1), W);
                                 y.y = __shfl_sync(0xffffffffu, y.y, (k + 1) & (W - 1), W);
                             }
@@ -743,6 +751,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         expm_minus_identity(Em, Tm, Dm, red);
                         TCB_ADD(16, te);
                     }
+#ifdef CS_TCB_CLOCKS
+                    if (!any_big) TCB_ADD(full ? 18 : 17, tpf);
+#endif
                     TCB_MARK(3);
                     // ---- (5) B operand (D~, hi | lo) and (6) update P += P D
                     build_bop<NT>(Dm, Bop);
