@@ -60,7 +60,7 @@ constexpr int MAXC = 16;
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
-__device__ unsigned long long g_tcb_cycles[24];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
+__device__ unsigned long long g_tcb_cycles[32];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
         if (tid == 0) {                                                              \
@@ -756,9 +756,16 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #endif
                     TCB_MARK(3);
                     // ---- (5) B operand (D~, hi | lo) and (6) update P += P D
+#ifdef CS_TCB_CLOCKS
+                    long long tu = clock64();
+#define TCB_UPD(i) do { TCB_ADD(i, tu); tu = clock64(); } while (0)
+#else
+#define TCB_UPD(i) do { } while (0)
+#endif
                     build_bop<NT>(Dm, Bop);
                     finish_v();       // the V rows of an incoming panel are needed from here
                     __syncthreads();  // D read before the ring (aliasing it) is written
+                    TCB_UPD(19);
                     // software pipeline over the 128-row M-blocks: stage lo(P) of block
                     // mb (both panels, the two 16 KB ring slots), issue its MMAs, then
                     // apply block mb-1's accumulator while the tensor core runs block mb
@@ -793,6 +800,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             ring_wait((mb - 1) & 1);  // block mb-1 done: lo slots free, accumulator ready
                             tc_after_sync();
                         }
+                        TCB_UPD(20);
 #pragma unroll
                         for (int i2 = 0; i2 < 2048 / NT; ++i2) {
                             const int u = tid + i2 * NT, at = u >> 10, w = u & 1023;
@@ -801,6 +809,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         }
                         fence_proxy_async_smem();
                         __syncthreads();
+                        TCB_UPD(21);
                         if (warp == (mb & 3)) {
                             if (lane == 0) {
                                 tc_after_sync();
@@ -824,9 +833,11 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             __syncwarp();
                         }
                         if (mb >= 1) epi(mb - 1);
+                        TCB_UPD(22);
                     }
                     ring_wait((K::MBLK - 1) & 1);
                     tc_after_sync();
+                    TCB_UPD(20);
                     TCB_MARK(4);
                     epi(K::MBLK - 1);
                     tc_before_sync();
@@ -1143,9 +1154,9 @@ size_t tcb_workspace(int mr, int nc, bool wantv) {
 #ifdef CS_TCB_CLOCKS
 extern "C" int cs_debug_tcb_cycles(unsigned long long *out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return 4;
-    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 24);
+    cudaMemcpyFromSymbol(out, tcb::g_tcb_cycles, sizeof(unsigned long long) * 32);
     if (reset) {
-        unsigned long long z[24] = {};
+        unsigned long long z[32] = {};
         cudaMemcpyToSymbol(tcb::g_tcb_cycles, z, sizeof(z));
     }
     return 0;

@@ -11,7 +11,7 @@ dev = torch.device("cuda:0")
 layer = configs.WORKLOADS[5].layers[0]
 wd = torch.from_numpy(configs.layer_weights(layer)).to(dev)
 L = _lib.load()
-buf = (ctypes.c_ulonglong * 24)()
+buf = (ctypes.c_ulonglong * 32)()
 lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 1)
 res = lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
@@ -29,3 +29,6 @@ print(f"  per matrix: load {buf[10] / nm:.0f}, verdicts {buf[11] / nm:.0f}, epil
 print(f"  rotating super-rounds: {buf[14] / n:.3f} product form, {buf[15] / n:.3f} exp form")
 print(f"  exp form: {buf[16] / max(buf[15], 1):.0f} cycles per call")
 print(f"  product form: {buf[17] / max(buf[14], 1):.0f} cycles per cross call (all product-form calls: {buf[14]}), full {buf[18]}")
+ru = max(buf[14] + buf[15], 1)
+print(f"  update per rotating super-round: bop+finish_v {buf[19] / ru:.0f}, MMA waits {buf[20] / ru:.0f}, "
+      f"lo staging {buf[21] / ru:.0f}, issue+epi {buf[22] / ru:.0f}")
