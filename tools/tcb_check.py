@@ -36,7 +36,12 @@ A = engine.symbol_field(wd, layer.n, layer.m, "f32", half=True, f_first=0, f_cou
 out["orthU"] = float(max(np.abs(u.conj().T @ u - np.eye(u.shape[1])).max() for u in U))
 out["orthV"] = float(max(np.abs(v.conj().T @ v - np.eye(v.shape[1])).max() for v in V))
 out["recon"] = float(max(np.abs((U[i] * sig[i]) @ V[i].conj().T - A[i]).max() / sig[i, 0] for i in range(len(U))))
-if os.environ.get("CS_TCB", "1") != "0":
+r64 = lfa_device(wd, layer.n, layer.m, "f64", True, u0=0, count=count, warm_start=warm, assemble=False)
+s64 = r64.sigma.cpu().numpy()
+out["max_rel_vs_f64"] = float((np.abs(sig - s64).max(axis=1) / s64[:, 0]).max())
+out["mean_rel_vs_f64"] = float((np.abs(sig - s64).max(axis=1) / s64[:, 0]).mean())
+del r64
+if os.environ.get("CS_TCB", "1") != "0" and not os.environ.get("CS_NO_SCALAR"):
     np.save("/tmp/sig_tcb.npy", sig)
     env = dict(os.environ, CS_TCB="0")
     subprocess.run([sys.executable, __file__, str(count), "1" if warm else "0"], env=env, check=True)
