@@ -60,7 +60,7 @@ constexpr int MAXC = 16;
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
-__device__ unsigned long long g_tcb_cycles[32];  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
+__device__ unsigned long long g_tcb_cycles[32];  // [23..28] exchange sub-phases  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
         if (tid == 0) {                                                              \
@@ -91,8 +91,10 @@ struct Ws {
     unsigned char *mail;  // per CTA [NBOX] outgoing panels
     int ngroups;
 };
-constexpr int CT_FX = 0, CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_META = 256, CT_BYTES = 512;
-// VERD/EPI/WORK: [2] by parity; META: [16] by exchange (the outgoing panel's modified / tested stamps)
+constexpr int CT_VERD = 96, CT_EPI = 160, CT_WORK = 192, CT_META = 256, CT_BYTES = 512;
+// VERD/EPI/WORK: [2] by parity; META: [16] 64-bit exchange flags by exchange number mod 16 -- low word the
+// exchange number (the outgoing panel is in its mailbox), high word the panel's modified / tested stamps
+// (16 bits each), so one release store publishes both and the receiver's acquire load returns both
 // mailboxes per CTA: exchange e writes mailbox e % NBOX.  A sweep has 2C-2
 // exchanges and ends with a group-wide verdict barrier, so a mailbox is
 // rewritten (NBOX >= 2C-1 exchanges later) only after every CTA of the group
@@ -148,6 +150,14 @@ __device__ __forceinline__ unsigned ld_acq(const void *p) {
 __device__ __forceinline__ void st_rel(void *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acq64(const void *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel64(void *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
@@ -173,6 +183,16 @@ __device__ __forceinline__ void spin_ge(const void *p, unsigned v, int what) {
         if (++n > (1u << 25)) spin_timeout(what);
         __nanosleep(32);
     }
+}
+// exchange flag: low word = the exchange number, high word = the panel's stamps
+__device__ __forceinline__ unsigned long long spin_ge64(const void *p, unsigned v, int what) {
+    unsigned n = 0;
+    unsigned long long x;
+    while ((int)((unsigned)(x = ld_acq64(p)) - v) < 0) {
+        if (++n > (1u << 25)) spin_timeout(what);
+        __nanosleep(32);
+    }
+    return x;
 }
 __device__ __forceinline__ unsigned spin_tag(const void *p, unsigned tag, int what) {
     unsigned n = 0, v;
@@ -500,7 +520,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const int o = (sc.ida[t2][rank] == ia) ? 1 : 0;
                 unsigned char *const outbox = box(rank, epoch + 1);
 
-                ++sr;
+                if (sr < 0xffffu) ++sr;  // stamps travel in 16 bits; saturated stamps never compare greater: no skips
                 const unsigned mod_max = mod_r[0] > mod_r[1] ? mod_r[0] : mod_r[1];
                 const bool skip = ctest[t] > mod_max && (!full || (wt_r[0] > mod_r[0] && wt_r[1] > mod_r[1]));
                 int any_rot = 0, any_big = 0;
@@ -858,22 +878,36 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     }
                     ++epoch;
                     __syncthreads();
+#ifdef CS_TCB_CLOCKS
+                    long long tx = clock64();
+#define TCB_XCH(i) do { TCB_ADD(i, tx); tx = clock64(); } while (0)
+                    if (tid == 0) { atomicAdd(&g_tcb_cycles[23], (unsigned long long)(tx - tcb_t)); }
+#else
+#define TCB_XCH(i) do { } while (0)
+#endif
                     if (tid == 0) {
-                        // one gpu-scope fence after the CTA barrier publishes every
-                        // thread's mailbox stores (the cooperative-groups grid-sync pattern)
-                        __threadfence();
+                        // the release store after the CTA barrier publishes every thread's
+                        // mailbox stores (release is cumulative over the barrier; one
+                        // MEMBAR.ALL.GPU -- a separate __threadfence() first is a second,
+                        // sequentially-consistent one: 2.6k cycles per exchange) together
+                        // with the panel's stamps
                         fence_proxy_async_global();
-                        unsigned *meta = reinterpret_cast<unsigned *>(myctl + CT_META + 8 * (epoch % 16));
-                        meta[0] = mod_r[o];
-                        meta[1] = wt_r[o];
-                        st_rel(myctl + CT_FX, epoch);
+                        st_rel64(myctl + CT_META + 8 * (epoch % 16),
+                                 (unsigned long long)epoch | ((unsigned long long)(mod_r[o] & 0xffffu) << 32) |
+                                     ((unsigned long long)(wt_r[o] & 0xffffu) << 48));
+                        TCB_XCH(24);
                         const unsigned char *in = box(src, epoch);
                         const uint32_t is = smem_u32(sm + sl[2] * SLOT);
-                        spin_ge(ctl(src) + CT_FX, epoch, 2);
-                        const unsigned *rm = reinterpret_cast<const unsigned *>(ctl(src) + CT_META + 8 * (epoch % 16));
-                        flags[4] = (int)__ldcg(rm);
-                        flags[5] = (int)__ldcg(rm + 1);
+#ifdef CS_TCB_CLOCKS
+                        if ((int)((unsigned)ld_acq64(ctl(src) + CT_META + 8 * (epoch % 16)) - epoch) < 0)
+                            atomicAdd(&g_tcb_cycles[28], 1ull);
+#endif
+                        const unsigned long long fx = spin_ge64(ctl(src) + CT_META + 8 * (epoch % 16), epoch, 2);
+                        TCB_XCH(25);
+                        flags[4] = (int)((fx >> 32) & 0xffffu);
+                        flags[5] = (int)(fx >> 48);
                         fence_proxy_async_global();
+                        TCB_XCH(26);
                         constexpr uint32_t XC = XBYTES / K::STAGES;  // the X rows of one Gram stage
 #pragma unroll
                         for (int c = 0; c < K::STAGES; ++c) {

@@ -32,3 +32,6 @@ print(f"  product form: {buf[17] / max(buf[14], 1):.0f} cycles per cross call (a
 ru = max(buf[14] + buf[15], 1)
 print(f"  update per rotating super-round: bop+finish_v {buf[19] / ru:.0f}, MMA waits {buf[20] / ru:.0f}, "
       f"lo staging {buf[21] / ru:.0f}, issue+epi {buf[22] / ru:.0f}")
+nx = max(n - nm * 7, 1)  # exchanges (the last super-round of a sweep has none; ~7 sweeps per matrix)
+print(f"  exchange split per exchange: outbox copy + CTA barrier {buf[23] / nx:.0f}, fence + publish {buf[24] / nx:.0f}, "
+      f"wait for the sender {buf[25] / nx:.0f} (not ready on arrival: {buf[28] / nx:.3f}), meta read {buf[26] / nx:.0f}")
