@@ -54,12 +54,21 @@ constexpr int NT = 512;
 #define CS_K3_TAU 0.35f  // measured: 0.05 2901 ms, 0.2 2722, 0.35 2666, 0.5 2689, never-exp 2728 (cfg5 warm SVD)
 #endif
 constexpr float K3_TAU = CS_K3_TAU;  // small-angle (product) vs large-angle (exp) combination
+#ifndef CS_K3_SPARSE
+#define CS_K3_SPARSE 32
+#endif
+// a super-round with at most this many rotating pairs (late sweeps) applies them
+// one after the other to the panels in shared memory instead of forming D and
+// running the tensor-core update (0: never)
+constexpr int K3_SPARSE = CS_K3_SPARSE;
+static_assert(K3_SPARSE <= 32, "the sparse list lives in the 64-word reduction scratch");
 constexpr int GW = 4;  // Gram-issuing warps (one TMEM accumulator each)
 constexpr int MAXC = 16;
 
 #ifdef CS_TCB_CLOCKS
 // experiment builds only (tools/ab_build.sh with CS_AB_FLAGS=-DCS_TCB_CLOCKS):
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
+__device__ unsigned long long g_tcb_sweep[4][16];  // per sweep index: cycles, super-rounds, dense rotating, sparse rotating
 __device__ unsigned long long g_tcb_cycles[32];  // [23..28] exchange sub-phases  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
@@ -506,6 +515,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const bool full = (i == 0);
 #ifdef CS_TCB_CLOCKS
                 long long tcb_t = clock64();
+                const long long tcb_t0 = tcb_t;
                 if (tid == 0) atomicAdd(&g_tcb_cycles[9], 1ull);
 #endif
                 unsigned char *const Pa = sm + sl[0] * SLOT;
@@ -523,7 +533,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 if (sr < 0xffffu) ++sr;  // stamps travel in 16 bits; saturated stamps never compare greater: no skips
                 const unsigned mod_max = mod_r[0] > mod_r[1] ? mod_r[0] : mod_r[1];
                 const bool skip = ctest[t] > mod_max && (!full || (wt_r[0] > mod_r[0] && wt_r[1] > mod_r[1]));
-                int any_rot = 0, any_big = 0;
+                int any_rot = 0, any_big = 0, nact = 0;
+                bool act_mine = false, mma_upd = false;  // this thread's pair rotates; the tensor-core update ran
                 Prm<float> *prm = reinterpret_cast<Prm<float> *>(RG + SC_PRM);
                 const int nround = full ? N2 - 1 : W;
                 TCB_MARK(7);
@@ -665,8 +676,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
                     prm[tid] = pm;
                 }
-                any_rot = __syncthreads_or(act > 0);
+                nact = __syncthreads_count(act > 0);
+                any_rot = nact > 0;
                 any_big = __syncthreads_or(act > 1);
+                act_mine = act > 0;
                 if (__syncthreads_or(act < 0)) bad = true;
                 ctest[t] = sr;
                 if (full) wt_r[0] = wt_r[1] = sr;
@@ -690,6 +703,47 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #ifdef CS_TCB_CLOCKS
                     const long long tpf = clock64();
 #endif
+                    if (K3_SPARSE > 0 && !any_big && nact <= K3_SPARSE) {
+                        // ---- (4s) a few rotating pairs (late sweeps): apply the rotations one
+                        // after the other, in round order, to the panels themselves -- the same
+                        // product Q of the rounds' rotations as (4a), without D and the
+                        // tensor-core update.  A thread owns its rows through all rotations.
+                        int *lst = reinterpret_cast<int *>(red);  // [0, 32) entries, [32, 48) per-warp counts
+                        const unsigned bal = __ballot_sync(0xffffffffu, act_mine);
+                        if (lane == 0) lst[32 + warp] = __popc(bal);
+                        __syncthreads();
+                        int base = 0;
+                        for (int w2 = 0; w2 < warp; ++w2) base += lst[32 + w2];
+                        if (act_mine) lst[base + __popc(bal & ((1u << lane) - 1u))] = tid;
+                        finish_v();
+                        __syncthreads();
+#pragma unroll 1
+                        for (int i2 = 0; i2 < nact; ++i2) {
+                            const int e = lst[i2];
+                            const Prm<float> pm = prm[e];
+                            int p, qq;
+                            inner_pair(full, e % W, e / W, p, qq);
+                            unsigned char *const cp = (p < W ? Pa : Pb), *const cq = (qq < W ? Pa : Pb);
+                            const int jp = 2 * (p & (W - 1)), jq = 2 * (qq & (W - 1));
+                            Rot<float> R;
+                            R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
+                            for (int row = tid; row < K::ROWS; row += NT) {
+                                float2 *xp = reinterpret_cast<float2 *>(cp + so(row, jp));
+                                float2 *yp = reinterpret_cast<float2 *>(cq + so(row, jq));
+                                float2 x = *xp, y = *yp;
+                                rot_apply<float>(x, y, R);
+                                *xp = x;
+                                *yp = y;
+                            }
+                        }
+                        __syncthreads();
+#ifdef CS_TCB_CLOCKS
+                        if (tid == 0) atomicAdd(&g_tcb_cycles[29], 1ull);
+                        TCB_ADD(30, tpf);
+#endif
+                        TCB_MARK(3);
+                    } else {
+                    mma_upd = true;
                     if (!any_big) {
                         // ---- (4a) small angles (every |gamma| / sqrt(alpha beta) <=
                         // GCHECK_TAU): D = Q - I for Q = the product of the rounds'
@@ -861,6 +915,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     TCB_MARK(4);
                     epi(K::MBLK - 1);
                     tc_before_sync();
+                    }  // tensor-core update
                 }
                 finish_v();
                 TCB_MARK(5);
@@ -870,7 +925,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 // from src's mailbox into the scratch slot
                 if (xchg) {
                     const int src = fwd ? sc.src[t][rank] : sc.dst[t2][rank];
-                    if (!(any_rot && !bad)) {
+                    if (!mma_upd) {
                         const float4 *sp = reinterpret_cast<const float4 *>(sm + sl[o] * SLOT);
                         float4 *dp = reinterpret_cast<float4 *>(outbox);
 #pragma unroll 4
@@ -934,6 +989,14 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     __syncthreads();
                 }
                 TCB_MARK(6);
+#ifdef CS_TCB_CLOCKS
+                if (tid == 0) {
+                    const int si = sweep < 15 ? sweep : 15;
+                    atomicAdd(&g_tcb_sweep[0][si], (unsigned long long)(clock64() - tcb_t0));
+                    atomicAdd(&g_tcb_sweep[1][si], 1ull);
+                    if (any_rot && !bad) atomicAdd(&g_tcb_sweep[mma_upd ? 2 : 3][si], 1ull);
+                }
+#endif
             }
             if (stop) break;
             // ---- post this sweep's verdict; the last allowed sweep collects it here
@@ -1192,6 +1255,15 @@ extern "C" int cs_debug_tcb_cycles(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long z[32] = {};
         cudaMemcpyToSymbol(tcb::g_tcb_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+extern "C" int cs_debug_tcb_sweeps(unsigned long long *out, int reset) {  // [4][16], see g_tcb_sweep
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    cudaMemcpyFromSymbol(out, tcb::g_tcb_sweep, sizeof(unsigned long long) * 64);
+    if (reset) {
+        unsigned long long z[64] = {};
+        cudaMemcpyToSymbol(tcb::g_tcb_sweep, z, sizeof(z));
     }
     return 0;
 }

@@ -14,6 +14,10 @@ L = _lib.load()
 buf = (ctypes.c_ulonglong * 32)()
 lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 1)
+sb = (ctypes.c_ulonglong * 64)()
+has_sw = hasattr(L, 'cs_debug_tcb_sweeps')
+if has_sw:
+    L.cs_debug_tcb_sweeps(sb, 1)
 res = lfa_device(wd, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=warm, assemble=False)
 L.cs_debug_tcb_cycles(buf, 0)
 n = buf[9]
@@ -35,3 +39,12 @@ print(f"  update per rotating super-round: bop+finish_v {buf[19] / ru:.0f}, MMA 
 nx = max(n - nm * 7, 1)  # exchanges (the last super-round of a sweep has none; ~7 sweeps per matrix)
 print(f"  exchange split per exchange: outbox copy + CTA barrier {buf[23] / nx:.0f}, fence + publish {buf[24] / nx:.0f}, "
       f"wait for the sender {buf[25] / nx:.0f} (not ready on arrival: {buf[28] / nx:.3f}), meta read {buf[26] / nx:.0f}")
+print(f"  sparse rotating super-rounds (rotations applied in place): {buf[29] / n:.3f} of all, {buf[30] / max(buf[29], 1):.0f} cycles each")
+if has_sw:
+    L.cs_debug_tcb_sweeps(sb, 0)
+    print("  by sweep: cycles per super-round, share of all cycles, dense / sparse rotating fraction, super-rounds per matrix")
+    allc = max(sum(sb[i] for i in range(16)), 1)
+    for i in range(16):
+        if sb[16 + i]:
+            print(f"    sweep {i + 1:2d}: {sb[i] / sb[16 + i]:7.0f}  {100 * sb[i] / allc:5.1f}%  dense {sb[32 + i] / sb[16 + i]:.3f} "
+                  f"sparse {sb[48 + i] / sb[16 + i]:.3f}  {sb[16 + i] / nm:6.2f}")
