@@ -70,9 +70,13 @@ constexpr int MAXC = 16;
 // CTA-0-thread-0 cycles per phase, summed over super-rounds
 __device__ unsigned long long g_tcb_sweep[4][16];  // per sweep index: cycles, super-rounds, dense rotating, sparse rotating
 __device__ unsigned long long g_tcb_cycles[32];  // [23..28] exchange sub-phases  // [9] super-round count, [10] load, [11] verdict, [12] epilogue, [13] matrices
+ // -DCS_TCB_CLOCKS_SWEEPS=n: the phase counters cover only the first n sweeps of a matrix
+#ifndef CS_TCB_CLOCKS_SWEEPS
+#define CS_TCB_CLOCKS_SWEEPS 1000
+#endif
 #define TCB_MARK(i)                                                                  \
     do {                                                                             \
-        if (tid == 0) {                                                              \
+        if (tid == 0 && tcb_on) {                                                              \
             const long long _c = clock64();                                          \
             atomicAdd(&g_tcb_cycles[i], (unsigned long long)(_c - tcb_t));           \
             tcb_t = _c;                                                              \
@@ -80,7 +84,7 @@ __device__ unsigned long long g_tcb_cycles[32];  // [23..28] exchange sub-phases
     } while (0)
 #define TCB_ADD(i, t0)                                                               \
     do {                                                                             \
-        if (tid == 0) atomicAdd(&g_tcb_cycles[i], (unsigned long long)(clock64() - (t0))); \
+        if (tid == 0 && tcb_on) atomicAdd(&g_tcb_cycles[i], (unsigned long long)(clock64() - (t0))); \
     } while (0)
 #else
 #define TCB_MARK(i) do { } while (0)
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         int sl[3] = {0, 1, 2};  // slots of panel a, panel b, scratch
         int ia = sc.ida[0][rank], ib = sc.idb[0][rank];
 #ifdef CS_TCB_CLOCKS
+        bool tcb_on = true;
         long long tcb_m = clock64();
         if (tid == 0) atomicAdd(&g_tcb_cycles[13], 1ull);
 #else
@@ -509,6 +514,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         for (int sweep = 0; sweep < a.max_sweeps && !stop; ++sweep) {
             const bool fwd = (sweep & 1) == 0;
             bool rot = false, bad = false;
+#ifdef CS_TCB_CLOCKS
+            tcb_on = sweep < CS_TCB_CLOCKS_SWEEPS;
+#endif
 #pragma unroll 1
             for (int i = 0; i < STEPS; ++i) {
                 const int t = fwd ? i : STEPS - 1 - i;
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #ifdef CS_TCB_CLOCKS
                 long long tcb_t = clock64();
                 const long long tcb_t0 = tcb_t;
-                if (tid == 0) atomicAdd(&g_tcb_cycles[9], 1ull);
+                if (tid == 0 && tcb_on) atomicAdd(&g_tcb_cycles[9], 1ull);
 #endif
                 unsigned char *const Pa = sm + sl[0] * SLOT;
                 unsigned char *const Pb = sm + sl[1] * SLOT;
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 if (any_rot && !bad) {
                     rot = true;
 #ifdef CS_TCB_CLOCKS
-                    if (tid == 0) atomicAdd(&g_tcb_cycles[any_big ? 15 : 14], 1ull);
+                    if (tid == 0 && tcb_on) atomicAdd(&g_tcb_cycles[any_big ? 15 : 14], 1ull);
 #endif
 #ifdef CS_TCB_CLOCKS
                     const long long tpf = clock64();
@@ -738,7 +746,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         }
                         __syncthreads();
 #ifdef CS_TCB_CLOCKS
-                        if (tid == 0) atomicAdd(&g_tcb_cycles[29], 1ull);
+                        if (tid == 0 && tcb_on) atomicAdd(&g_tcb_cycles[29], 1ull);
                         TCB_ADD(30, tpf);
 #endif
                         TCB_MARK(3);
@@ -936,26 +944,30 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #ifdef CS_TCB_CLOCKS
                     long long tx = clock64();
 #define TCB_XCH(i) do { TCB_ADD(i, tx); tx = clock64(); } while (0)
-                    if (tid == 0) { atomicAdd(&g_tcb_cycles[23], (unsigned long long)(tx - tcb_t)); }
+                    if (tid == 0 && tcb_on) { atomicAdd(&g_tcb_cycles[23], (unsigned long long)(tx - tcb_t)); }
 #else
 #define TCB_XCH(i) do { } while (0)
 #endif
-                    if (tid == 0) {
+                    if (tid == 32) {
                         // the release store after the CTA barrier publishes every thread's
                         // mailbox stores (release is cumulative over the barrier; one
                         // MEMBAR.ALL.GPU -- a separate __threadfence() first is a second,
                         // sequentially-consistent one: 2.6k cycles per exchange) together
-                        // with the panel's stamps
+                        // with the panel's stamps.  It waits ~1.6k cycles for the stores to
+                        // drain, so a thread of another warp does it while thread 0 already
+                        // waits for the sender.
                         fence_proxy_async_global();
                         st_rel64(myctl + CT_META + 8 * (epoch % 16),
                                  (unsigned long long)epoch | ((unsigned long long)(mod_r[o] & 0xffffu) << 32) |
                                      ((unsigned long long)(wt_r[o] & 0xffffu) << 48));
+                    }
+                    if (tid == 0) {
                         TCB_XCH(24);
                         const unsigned char *in = box(src, epoch);
                         const uint32_t is = smem_u32(sm + sl[2] * SLOT);
 #ifdef CS_TCB_CLOCKS
                         if ((int)((unsigned)ld_acq64(ctl(src) + CT_META + 8 * (epoch % 16)) - epoch) < 0)
-                            atomicAdd(&g_tcb_cycles[28], 1ull);
+                            if (tcb_on) atomicAdd(&g_tcb_cycles[28], 1ull);
 #endif
                         const unsigned long long fx = spin_ge64(ctl(src) + CT_META + 8 * (epoch % 16), epoch, 2);
                         TCB_XCH(25);
