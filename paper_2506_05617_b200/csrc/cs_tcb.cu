@@ -500,10 +500,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #ifdef CS_TCB_CLOCKS
             const long long tv = clock64();
 #endif
-            if (tid == 0) {
-                unsigned any = 0;
-                for (int d = 0; d < C; ++d) any |= spin_tag(ctl(d) + CT_VERD + 4 * (vseq & 1), vseq, 4);
-                flags[0] = (int)(any & 3u);
+            if (warp == 0) {  // lane d polls CTA d: the C acquire loads overlap
+                unsigned any = lane < C ? spin_tag(ctl(lane) + CT_VERD + 4 * (vseq & 1), vseq, 4) : 0u;
+                any = __reduce_or_sync(0xffffffffu, any);
+                if (lane == 0) flags[0] = (int)(any & 3u);
             }
             __syncthreads();
             const int v = flags[0];
@@ -1046,7 +1046,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         if (tid == 0) {
             __threadfence();
             st_rel(myctl + CT_EPI + 4 * (mseq & 1), mseq);
-            for (int d = 0; d < C; ++d) spin_ge(ctl(d) + CT_EPI + 4 * (mseq & 1), mseq, 5);
+        }
+        if (warp == 0) {
+            __syncwarp();
+            if (lane < C) spin_ge(ctl(lane) + CT_EPI + 4 * (mseq & 1), mseq, 5);
         }
         __syncthreads();
         for (int j = tid; j < NC; j += NT) sig2[j] = sqrtf(__ldcg(gs + j));
