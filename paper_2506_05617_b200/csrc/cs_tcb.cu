@@ -663,10 +663,14 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                             Gm[c * LDG + c] = make_float2(nrm(2 * c) + nrm(2 * c + 1), 0.f);
                         }
                     }
+                    if (tid == 0) flags[6] = 0;  // the angles' block-wide tallies
                     __syncthreads();
                 }
-                for (int x = tid; x < N2 * LDG; x += NT) Dm[x] = make_float2(0.f, 0.f);
-                __syncthreads();
+                // D starts from zero only where it is accumulated (the full rounds' product
+                // form); the cross product form and exp(E) write every entry.  The tally
+                // barrier below orders this before D is used.
+                if (full)
+                    for (int x = tid; x < N2 * LDG; x += NT) Dm[x] = make_float2(0.f, 0.f);
                 TCB_MARK(1);
                 // ---- (3) every pair's rotation from G at once (the reference's test
                 // and root, rot_params), slot k of round r at prm[16 r + k]
@@ -684,11 +688,21 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
                     prm[tid] = pm;
                 }
-                nact = __syncthreads_count(act > 0);
-                any_rot = nact > 0;
-                any_big = __syncthreads_or(act > 1);
-                act_mine = act > 0;
-                if (__syncthreads_or(act < 0)) bad = true;
+                {
+                    // one barrier for the three block-wide tallies: rotating pairs (bits 0..15),
+                    // warps with a large angle (16..23), warps with a non-finite pair (24..31)
+                    const unsigned brot = __ballot_sync(0xffffffffu, act > 0);
+                    const int wbig = __any_sync(0xffffffffu, act > 1), wbad = __any_sync(0xffffffffu, act < 0);
+                    const int tally = __popc(brot) + (wbig << 16) + (wbad << 24);
+                    if (lane == 0 && tally) atomicAdd(&flags[6], tally);
+                    __syncthreads();
+                    const int all = flags[6];
+                    nact = all & 0xffff;
+                    any_rot = nact > 0;
+                    any_big = (all >> 16) & 0xff;
+                    act_mine = act > 0;
+                    if (all >> 24) bad = true;
+                }
                 ctest[t] = sr;
                 if (full) wt_r[0] = wt_r[1] = sr;
                 if (any_rot && !bad) mod_r[0] = mod_r[1] = sr;
