@@ -859,23 +859,43 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #define TCB_UPD(i) do { } while (0)
 #endif
                     build_bop<NT>(Dm, Bop);
-                    finish_v();       // the V rows of an incoming panel are needed from here
-                    __syncthreads();  // D read before the ring (aliasing it) is written
+                    finish_v();  // the V rows of an incoming panel are needed from here
                     TCB_UPD(19);
-                    // software pipeline over the 128-row M-blocks: stage lo(P) of block
-                    // mb (both panels, the two 16 KB ring slots), issue its MMAs, then
-                    // apply block mb-1's accumulator while the tensor core runs block mb
-                    // (its MMAs read the hi words straight from the panels, so block
-                    // mb-1's rows are rewritten only after its MMAs completed).  Each
-                    // block's MMA stream comes from its own warp: one warp's stream
-                    // completes ~285 cycles per MMA, streams of different warps overlap
-                    // (tools/tc_rate_probe.cu).
+                    // software pipeline over the 128-row M-blocks: lo(P) of block mb (both
+                    // panels) goes from registers into TENSOR MEMORY (tcgen05.st) and is
+                    // the A operand of the lo(P) hi(D~) MMAs from there -- shared memory is
+                    // the bound of this phase (a K = 8 tf32 MMA with M = 128, N = 128 reads
+                    // 8 KB per 64 cycles, the whole 128 B/cycle), so the staged copy's 32 KB
+                    // written and 32 KB re-read per block are what this saves.  Block mb's
+                    // MMAs are issued, then block mb-1's accumulator is applied while the
+                    // tensor core runs block mb (its MMAs read the hi words straight from
+                    // the panels, so block mb-1's rows are rewritten only after its MMAs
+                    // completed).  TMEM: two accumulators [0, 256) and two lo(P) blocks
+                    // [256, 384), alternating by block.  Each block's MMA stream comes from
+                    // its own warp (tools/tc_rate_probe.cu).
+                    constexpr uint32_t TM_LO = 256;
+                    auto stage_lo = [&](int mb) {
+                        // quarter q = TMEM lanes (rows), warp group c = 16 real columns of the pair
+                        const int q = warp & 3, c = warp >> 2;
+                        const int row = mb * 128 + 32 * q + lane;
+                        const unsigned char *P = (c >> 1) ? Pb : Pa;
+                        uint32_t rr[16];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float4 l = lo4(*reinterpret_cast<const float4 *>(P + so4(row, 4 * (c & 1) + u)));
+                            rr[4 * u] = __float_as_uint(l.x);
+                            rr[4 * u + 1] = __float_as_uint(l.y);
+                            rr[4 * u + 2] = __float_as_uint(l.z);
+                            rr[4 * u + 3] = __float_as_uint(l.w);
+                        }
+                        tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + TM_LO + 64 * (mb & 1) + 16 * c, rr);
+                    };
                     auto epi = [&](int mb) {
                         // quarter q = TMEM lanes (rows), warp group c = 16 output real columns
                         const int q = warp & 3, c = warp >> 2;
                         const int row = mb * 128 + 32 * q + lane;
                         float v[16], vc[16];
-                        tmem_ld16x2(tmem + ((uint32_t)(32 * q) << 16) + 128 * mb + 16 * c, v, vc);
+                        tmem_ld16x2(tmem + ((uint32_t)(32 * q) << 16) + 128 * (mb & 1) + 16 * c, v, vc);
 #pragma unroll
                         for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
 #pragma unroll
@@ -893,35 +913,31 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #pragma unroll 1
                     for (int mb = 0; mb < K::MBLK; ++mb) {
                         if (mb >= 1) {
-                            ring_wait((mb - 1) & 1);  // block mb-1 done: lo slots free, accumulator ready
+                            ring_wait((mb - 1) & 1);  // block mb-1 done: its accumulator is ready
                             tc_after_sync();
                         }
                         TCB_UPD(20);
-#pragma unroll
-                        for (int i2 = 0; i2 < 2048 / NT; ++i2) {
-                            const int u = tid + i2 * NT, at = u >> 10, w = u & 1023;
-                            *reinterpret_cast<float4 *>(RG + at * 16384 + 16 * w) =
-                                lo4(*reinterpret_cast<const float4 *>((at ? Pb : Pa) + mb * 16384 + 16 * w));
-                        }
-                        fence_proxy_async_smem();
+                        stage_lo(mb);  // block mb-2's MMAs (the last readers of this lo block) completed a block ago
+                        if (mb == 0) fence_proxy_async_smem();  // the B operand
+                        tc_before_sync();
                         __syncthreads();
                         TCB_UPD(21);
                         if (warp == (mb & 3)) {
                             if (lane == 0) {
                                 tc_after_sync();
-                                const uint32_t d = tmem + 128 * mb;
+                                const uint32_t d = tmem + 128 * (mb & 1), lo = tmem + TM_LO + 64 * (mb & 1);
 #pragma unroll
                                 for (int at = 0; at < 2; ++at) {
                                     const uint32_t ah = smem_u32((at ? Pb : Pa) + mb * 16384);
-                                    const uint32_t al = smem_u32(RG + at * 16384);
                                     const uint32_t bb = smem_u32(Bop) + at * 16384;
 #pragma unroll
                                     for (int ks = 0; ks < 4; ++ks) {
-                                        const uint64_t dah = desc_sw128(ah + ks * 32), dal = desc_sw128(al + ks * 32);
+                                        const uint64_t dah = desc_sw128(ah + ks * 32);
                                         const uint64_t db = desc_sw128(bb + ks * 32);
                                         const uint32_t acc0 = (at | ks) ? 1u : 0u;
-                                        mma_tf32(d, dah, db, IDESC_UPD, acc0);        // [hi*hi | hi*lo]
-                                        mma_tf32(d + 64, dal, db, IDESC_UPD_LO, 1u);  // + lo*hi -> correction
+                                        mma_tf32(d, dah, db, IDESC_UPD, acc0);  // [hi*hi | hi*lo]
+                                        // + lo*hi -> correction (A = lo(P) in tensor memory)
+                                        mma_tf32_ts(d + 64, lo + 32 * at + 8 * ks, db, IDESC_UPD_LO, 1u);
                                     }
                                 }
                                 mma_commit(&bar[mb & 1]);
