@@ -861,34 +861,43 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     build_bop<NT>(Dm, Bop);
                     finish_v();  // the V rows of an incoming panel are needed from here
                     TCB_UPD(19);
-                    // software pipeline over the 128-row M-blocks: lo(P) of block mb (both
-                    // panels) goes from registers into TENSOR MEMORY (tcgen05.st) and is
-                    // the A operand of the lo(P) hi(D~) MMAs from there -- shared memory is
-                    // the bound of this phase (a K = 8 tf32 MMA with M = 128, N = 128 reads
-                    // 8 KB per 64 cycles, the whole 128 B/cycle), so the staged copy's 32 KB
-                    // written and 32 KB re-read per block are what this saves.  Block mb's
-                    // MMAs are issued, then block mb-1's accumulator is applied while the
-                    // tensor core runs block mb (its MMAs read the hi words straight from
-                    // the panels, so block mb-1's rows are rewritten only after its MMAs
-                    // completed).  TMEM: two accumulators [0, 256) and two lo(P) blocks
-                    // [256, 384), alternating by block.  Each block's MMA stream comes from
-                    // its own warp (tools/tc_rate_probe.cu).
+                    // software pipeline over the 128-row M-blocks.  The A operands -- the
+                    // panel rows themselves (the tensor core truncates the fp32 word to tf32:
+                    // "hi") and lo(P) -- go from registers into TENSOR MEMORY (tcgen05.st) and
+                    // the MMAs read them from there: shared memory is the bound of this phase
+                    // (a K = 8 tf32 MMA with M = N = 128 and both operands in shared memory
+                    // reads 8 KB per 64 cycles, the whole 128 B/cycle of the SM), so a staged
+                    // shared-memory copy of lo(P) (32 KB written and re-read per block) and
+                    // the MMAs' own reads of the panel rows are what this saves; only the B
+                    // operand (D~, 6 KB per K-step pair) still comes from shared memory.
+                    // Block mb is staged and its MMAs issued while block mb-1's still run;
+                    // then block mb-1's accumulator is applied to the panels (its rows are
+                    // rewritten only after its own MMAs completed).  TMEM: two accumulators
+                    // [0, 256) and two operand blocks [256, 512) (hi | lo, 64 columns each),
+                    // alternating by block.  Each block's MMA stream comes from its own warp
+                    // (tools/tc_rate_probe.cu).
                     constexpr uint32_t TM_LO = 256;
                     auto stage_lo = [&](int mb) {
                         // quarter q = TMEM lanes (rows), warp group c = 16 real columns of the pair
                         const int q = warp & 3, c = warp >> 2;
                         const int row = mb * 128 + 32 * q + lane;
                         const unsigned char *P = (c >> 1) ? Pb : Pa;
-                        uint32_t rr[16];
+                        uint32_t hh[16], rr[16];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const float4 l = lo4(*reinterpret_cast<const float4 *>(P + so4(row, 4 * (c & 1) + u)));
+                            const float4 x = *reinterpret_cast<const float4 *>(P + so4(row, 4 * (c & 1) + u));
+                            const float4 l = lo4(x);
+                            hh[4 * u] = __float_as_uint(x.x);  // the raw word: the tensor core truncates it to tf32
+                            hh[4 * u + 1] = __float_as_uint(x.y);
+                            hh[4 * u + 2] = __float_as_uint(x.z);
+                            hh[4 * u + 3] = __float_as_uint(x.w);
                             rr[4 * u] = __float_as_uint(l.x);
                             rr[4 * u + 1] = __float_as_uint(l.y);
                             rr[4 * u + 2] = __float_as_uint(l.z);
                             rr[4 * u + 3] = __float_as_uint(l.w);
                         }
-                        tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + TM_LO + 64 * (mb & 1) + 16 * c, rr);
+                        const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + TM_LO + 128 * (mb & 1) + 16 * c;
+                        tmem_st16x2(t0, hh, t0 + 64, rr);
                     };
                     auto epi = [&](int mb) {
                         // quarter q = TMEM lanes (rows), warp group c = 16 output real columns
@@ -912,12 +921,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     };
 #pragma unroll 1
                     for (int mb = 0; mb < K::MBLK; ++mb) {
-                        if (mb >= 1) {
-                            ring_wait((mb - 1) & 1);  // block mb-1 done: its accumulator is ready
-                            tc_after_sync();
-                        }
-                        TCB_UPD(20);
-                        stage_lo(mb);  // block mb-2's MMAs (the last readers of this lo block) completed a block ago
+                        // block mb-2's MMAs (the last readers of this TMEM operand block) completed and its
+                        // accumulator was applied a block ago; block mb-1's may still be running
+                        stage_lo(mb);
                         if (mb == 0) fence_proxy_async_smem();  // the B operand
                         tc_before_sync();
                         __syncthreads();
@@ -925,27 +931,31 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         if (warp == (mb & 3)) {
                             if (lane == 0) {
                                 tc_after_sync();
-                                const uint32_t d = tmem + 128 * (mb & 1), lo = tmem + TM_LO + 64 * (mb & 1);
+                                const uint32_t d = tmem + 128 * (mb & 1), hi = tmem + TM_LO + 128 * (mb & 1), lo = hi + 64;
 #pragma unroll
                                 for (int at = 0; at < 2; ++at) {
-                                    const uint32_t ah = smem_u32((at ? Pb : Pa) + mb * 16384);
                                     const uint32_t bb = smem_u32(Bop) + at * 16384;
 #pragma unroll
                                     for (int ks = 0; ks < 4; ++ks) {
-                                        const uint64_t dah = desc_sw128(ah + ks * 32);
                                         const uint64_t db = desc_sw128(bb + ks * 32);
                                         const uint32_t acc0 = (at | ks) ? 1u : 0u;
-                                        mma_tf32(d, dah, db, IDESC_UPD, acc0);  // [hi*hi | hi*lo]
-                                        // + lo*hi -> correction (A = lo(P) in tensor memory)
-                                        mma_tf32_ts(d + 64, lo + 32 * at + 8 * ks, db, IDESC_UPD_LO, 1u);
+                                        // A = P and lo(P) in tensor memory, B = [hi(D~) | lo(D~)] in shared memory
+                                        mma_tf32_ts(d, hi + 32 * at + 8 * ks, db, IDESC_UPD, acc0);        // [hi*hi | hi*lo]
+                                        mma_tf32_ts(d + 64, lo + 32 * at + 8 * ks, db, IDESC_UPD_LO, 1u);  // + lo*hi -> correction
                                     }
                                 }
                                 mma_commit(&bar[mb & 1]);
                             }
                             __syncwarp();
                         }
-                        if (mb >= 1) epi(mb - 1);
                         TCB_UPD(22);
+                        if (mb >= 1) {
+                            ring_wait((mb - 1) & 1);  // block mb-1 done: its accumulator is ready
+                            tc_after_sync();
+                            TCB_UPD(20);
+                            epi(mb - 1);
+                            TCB_UPD(22);
+                        }
                     }
                     ring_wait((K::MBLK - 1) & 1);
                     tc_after_sync();
