@@ -860,109 +860,118 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #endif
                     build_bop<NT>(Dm, Bop);
                     finish_v();  // the V rows of an incoming panel are needed from here
+                    fence_proxy_async_smem();  // the B operand is read by the tensor core
+                    __syncthreads();
                     TCB_UPD(19);
-                    // software pipeline over the 128-row M-blocks.  The A operands -- the
-                    // panel rows themselves (the tensor core truncates the fp32 word to tf32:
-                    // "hi") and lo(P) -- go from registers into TENSOR MEMORY (tcgen05.st) and
-                    // the MMAs read them from there: shared memory is the bound of this phase
-                    // (a K = 8 tf32 MMA with M = N = 128 and both operands in shared memory
-                    // reads 8 KB per 64 cycles, the whole 128 B/cycle of the SM), so a staged
-                    // shared-memory copy of lo(P) (32 KB written and re-read per block) and
-                    // the MMAs' own reads of the panel rows are what this saves; only the B
-                    // operand (D~, 6 KB per K-step pair) still comes from shared memory.
-                    // Block mb is staged and its MMAs issued while block mb-1's still run;
-                    // then block mb-1's accumulator is applied to the panels (its rows are
-                    // rewritten only after its own MMAs completed).  TMEM: two accumulators
-                    // [0, 256) and two operand blocks [256, 512) (hi | lo, 64 columns each),
-                    // alternating by block.  Each block's MMA stream comes from its own warp
-                    // (tools/tc_rate_probe.cu).
-                    constexpr uint32_t TM_LO = 256;
-                    auto stage_lo = [&](int mb) {
-                        // quarter q = TMEM lanes (rows), warp group c = 16 real columns of the pair
-                        const int q = warp & 3, c = warp >> 2;
-                        const int row = mb * 128 + 32 * q + lane;
-                        const unsigned char *P = (c >> 1) ? Pb : Pa;
-                        uint32_t hh[16], rr[16];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const float4 x = *reinterpret_cast<const float4 *>(P + so4(row, 4 * (c & 1) + u));
-                            const float4 l = lo4(x);
-                            hh[4 * u] = __float_as_uint(x.x);  // the raw word: the tensor core truncates it to tf32
-                            hh[4 * u + 1] = __float_as_uint(x.y);
-                            hh[4 * u + 2] = __float_as_uint(x.z);
-                            hh[4 * u + 3] = __float_as_uint(x.w);
-                            rr[4 * u] = __float_as_uint(l.x);
-                            rr[4 * u + 1] = __float_as_uint(l.y);
-                            rr[4 * u + 2] = __float_as_uint(l.z);
-                            rr[4 * u + 3] = __float_as_uint(l.w);
-                        }
-                        const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + TM_LO + 128 * (mb & 1) + 16 * c;
-                        tmem_st16x2(t0, hh, t0 + 64, rr);
-                    };
-                    auto epi = [&](int mb) {
-                        // quarter q = TMEM lanes (rows), warp group c = 16 output real columns
-                        const int q = warp & 3, c = warp >> 2;
-                        const int row = mb * 128 + 32 * q + lane;
-                        float v[16], vc[16];
-                        tmem_ld16x2(tmem + ((uint32_t)(32 * q) << 16) + 128 * (mb & 1) + 16 * c, v, vc);
-#pragma unroll
-                        for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int k4 = 4 * c + u, role = k4 >> 3;
-                            const uint32_t off = so4(row, k4 & 7);
-                            float4 *pp = reinterpret_cast<float4 *>((role ? Pb : Pa) + off);
-                            float4 x = *pp;
-                            x.x += v[4 * u]; x.y += v[4 * u + 1]; x.z += v[4 * u + 2]; x.w += v[4 * u + 3];
-                            // the outgoing panel goes straight to the mailbox (same layout)
-                            if (xchg && role == o) __stcg(reinterpret_cast<float4 *>(outbox + off), x);
-                            else *pp = x;
-                        }
-                    };
+                    // Warp-specialised pipeline over the 128-row M-blocks.  The A operands --
+                    // the panel rows themselves (the tensor core truncates the fp32 word to
+                    // tf32: "hi") and lo(P) -- go from registers into TENSOR MEMORY
+                    // (tcgen05.st) and the MMAs read them from there: shared memory is the
+                    // bound of the MMAs (K = 8 tf32, M = N = 128 with both operands in shared
+                    // memory reads 8 KB per 64 cycles, the SM's whole 128 B/cycle), so a
+                    // staged shared-memory copy of lo(P) (32 KB written and re-read per
+                    // block) and the MMAs' own reads of the panel rows are what this saves;
+                    // only the B operand (D~) still comes from shared memory.
+                    //   warps 0-7 (stagers): block mb's operands -> TMEM, then one of them
+                    //     issues its MMAs (each block's stream from its own warp,
+                    //     tools/tc_rate_probe.cu);
+                    //   warps 8-15 (epilogue): wait for block mb's MMAs, add its accumulator
+                    //     (main + correction) to the panels -- the outgoing panel straight
+                    //     to the mailbox.  TMEM reads run at 64 B/cycle (64 KB per block:
+                    //     ~1k cycles), which the stagers' work now overlaps.
+                    // TMEM: two accumulators [0, 256) and two operand blocks [256, 512)
+                    // (hi | lo, 64 columns each), alternating by block.  A block's operands
+                    // are restaged after its MMAs completed (mbarrier), an accumulator is
+                    // overwritten after the epilogue warps read it (named barrier 2 + slot).
+                    // bar[0/1] see two commits per update, so their phase parity at the
+                    // start of an update is always 0: block mb completes phase (mb >> 1) & 1.
+                    static_assert(K::MBLK == 4 && NT == 512, "update pipeline: 4 blocks, 8 + 8 warps");
+                    constexpr uint32_t TM_OP = 256;
+                    const int q = warp & 3, hsel = (warp >> 2) & 1;  // TMEM lane quarter; panel a / b (32 real columns)
+                    unsigned char *const Ph = hsel ? Pb : Pa;
+                    if (warp < 8) {
 #pragma unroll 1
-                    for (int mb = 0; mb < K::MBLK; ++mb) {
-                        // block mb-2's MMAs (the last readers of this TMEM operand block) completed and its
-                        // accumulator was applied a block ago; block mb-1's may still be running
-                        stage_lo(mb);
-                        if (mb == 0) fence_proxy_async_smem();  // the B operand
-                        tc_before_sync();
-                        __syncthreads();
-                        TCB_UPD(21);
-                        if (warp == (mb & 3)) {
-                            if (lane == 0) {
-                                tc_after_sync();
-                                const uint32_t d = tmem + 128 * (mb & 1), hi = tmem + TM_LO + 128 * (mb & 1), lo = hi + 64;
-#pragma unroll
-                                for (int at = 0; at < 2; ++at) {
-                                    const uint32_t bb = smem_u32(Bop) + at * 16384;
-#pragma unroll
-                                    for (int ks = 0; ks < 4; ++ks) {
-                                        const uint64_t db = desc_sw128(bb + ks * 32);
-                                        const uint32_t acc0 = (at | ks) ? 1u : 0u;
-                                        // A = P and lo(P) in tensor memory, B = [hi(D~) | lo(D~)] in shared memory
-                                        mma_tf32_ts(d, hi + 32 * at + 8 * ks, db, IDESC_UPD, acc0);        // [hi*hi | hi*lo]
-                                        mma_tf32_ts(d + 64, lo + 32 * at + 8 * ks, db, IDESC_UPD_LO, 1u);  // + lo*hi -> correction
-                                    }
-                                }
-                                mma_commit(&bar[mb & 1]);
-                            }
-                            __syncwarp();
-                        }
-                        TCB_UPD(22);
-                        if (mb >= 1) {
-                            ring_wait((mb - 1) & 1);  // block mb-1 done: its accumulator is ready
-                            tc_after_sync();
+                        for (int mb = 0; mb < K::MBLK; ++mb) {
+                            if (mb >= 2) mbar_wait(&bar[mb & 1], 0);  // block mb-2's MMAs done: its operand block is free
                             TCB_UPD(20);
-                            epi(mb - 1);
+                            const int row = mb * 128 + 32 * q + lane;
+                            const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + TM_OP + 128 * (mb & 1) + 32 * hsel;
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                uint32_t hh[16], rr[16];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const float4 x = *reinterpret_cast<const float4 *>(Ph + so4(row, 4 * hf + u));
+                                    const float4 l = lo4(x);
+                                    hh[4 * u] = __float_as_uint(x.x);  // the raw word: the tensor core truncates it
+                                    hh[4 * u + 1] = __float_as_uint(x.y);
+                                    hh[4 * u + 2] = __float_as_uint(x.z);
+                                    hh[4 * u + 3] = __float_as_uint(x.w);
+                                    rr[4 * u] = __float_as_uint(l.x);
+                                    rr[4 * u + 1] = __float_as_uint(l.y);
+                                    rr[4 * u + 2] = __float_as_uint(l.z);
+                                    rr[4 * u + 3] = __float_as_uint(l.w);
+                                }
+                                tmem_st16_nowait(t0 + 16 * hf, hh);
+                                tmem_st16_nowait(t0 + 64 + 16 * hf, rr);
+                            }
+                            tmem_st_wait();
+                            tc_before_sync();
+                            named_sync(1, 256);  // the stagers
+                            if (mb >= 2) named_sync(2 + (mb & 1), NT);  // the epilogue warps read accumulator mb & 1 (block mb-2)
+                            TCB_UPD(21);
+                            if (warp == mb) {
+                                if (lane == 0) {
+                                    tc_after_sync();
+                                    const uint32_t d = tmem + 128 * (mb & 1), hi = tmem + TM_OP + 128 * (mb & 1), lo = hi + 64;
+#pragma unroll
+                                    for (int at = 0; at < 2; ++at) {
+                                        const uint32_t bb = smem_u32(Bop) + at * 16384;
+#pragma unroll
+                                        for (int ks = 0; ks < 4; ++ks) {
+                                            const uint64_t db = desc_sw128(bb + ks * 32);
+                                            const uint32_t acc0 = (at | ks) ? 1u : 0u;
+                                            mma_tf32_ts(d, hi + 32 * at + 8 * ks, db, IDESC_UPD, acc0);        // [hi*hi | hi*lo]
+                                            mma_tf32_ts(d + 64, lo + 32 * at + 8 * ks, db, IDESC_UPD_LO, 1u);  // + lo*hi -> correction
+                                        }
+                                    }
+                                    mma_commit(&bar[mb & 1]);
+                                }
+                                __syncwarp();
+                            }
                             TCB_UPD(22);
                         }
+                    } else {
+#pragma unroll 1
+                        for (int mb = 0; mb < K::MBLK; ++mb) {
+                            mbar_wait(&bar[mb & 1], (uint32_t)(mb >> 1) & 1u);  // block mb's MMAs done
+                            tc_after_sync();
+                            const int row = mb * 128 + 32 * q + lane;
+                            const bool out = xchg && hsel == o;  // the outgoing panel goes straight to the mailbox (same layout)
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                float v[16], vc[16];
+                                tmem_ld16x2(tmem + ((uint32_t)(32 * q) << 16) + 128 * (mb & 1) + 32 * hsel + 16 * hf, v, vc);
+#pragma unroll
+                                for (int i2 = 0; i2 < 16; ++i2) v[i2] += vc[i2];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const uint32_t off = so4(row, 4 * hf + u);
+                                    float4 *pp = reinterpret_cast<float4 *>(Ph + off);
+                                    float4 x = *pp;
+                                    x.x += v[4 * u]; x.y += v[4 * u + 1]; x.z += v[4 * u + 2]; x.w += v[4 * u + 3];
+                                    if (out) __stcg(reinterpret_cast<float4 *>(outbox + off), x);
+                                    else *pp = x;
+                                }
+                            }
+                            if (mb < 2) {
+                                tc_before_sync();
+                                named_arrive(2 + (mb & 1), NT);  // accumulator mb & 1 may be overwritten (block mb+2)
+                            }
+                        }
+                        tc_before_sync();
                     }
-                    ring_wait((K::MBLK - 1) & 1);
-                    tc_after_sync();
-                    TCB_UPD(20);
                     TCB_MARK(4);
-                    epi(K::MBLK - 1);
-                    tc_before_sync();
                     }  // tensor-core update
                 }
                 finish_v();
