@@ -132,3 +132,30 @@ def test_cfg5_lazy_partner_triplets(cuda):
     _, trip_h = host(fld, values_only=False)
     t = trip_h[fs[-1]]
     assert isinstance(t.U, np.ndarray) and t.U.dtype == np.complex128 and t.U.shape == (256, 256)
+
+
+def test_tensor_core_kernel_matches_scalar_kernel(cuda, monkeypatch):
+    """K3 (tensor-core blocked Jacobi: TMEM-fed, warp-specialised update)
+    against K2 (scalar panel kernel, CS_TCB=0) on the same warm-started cfg5
+    blocks: sigma within 2e-6 of sigma_max, the energy identity
+    sum sigma^2 = ||A||_F^2, orthonormal U / V and A V = U diag(sigma)
+    (CS/blocksvd.py:155-173 is what both replace)."""
+    layer = configs.WORKLOADS[5].layers[0]
+    w = _w(layer, cuda, "f32")
+    count = 1024  # four full rows of the half grid (whole warm-start trees; seven rounds of the work queue)
+    k3 = lfa_device(w, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=True, assemble=False)
+    monkeypatch.setenv("CS_TCB", "0")
+    k2 = lfa_device(w, layer.n, layer.m, "f32", True, u0=0, count=count, warm_start=True, assemble=False)
+    monkeypatch.delenv("CS_TCB")
+    assert (k3.info > 0).all() and (k2.info > 0).all()
+    s3, s2 = k3.sigma.cpu().numpy(), k2.sigma.cpu().numpy()
+    assert per_freq_rel_err(s3, s2).max() <= 2e-6
+    A = engine.symbol_field(w, layer.n, layer.m, "f32", half=True, f_first=0, f_count=count)
+    fro = (A.abs().double() ** 2).sum(dim=(1, 2)).cpu().numpy()
+    energy = np.abs((s3.astype(np.float64) ** 2).sum(axis=1) - fro) / fro
+    assert energy.max() <= 5e-6
+    eye = torch.eye(layer.c_in, device=cuda, dtype=torch.complex64)
+    for F in (k3.U, k3.V):
+        assert (F.mH @ F - eye).abs().amax().item() <= 2e-5
+    res = (A @ k3.V - k3.U * k3.sigma[:, None, :].to(torch.complex64)).abs().amax(dim=(1, 2))
+    assert (res / k3.sigma[:, 0]).max().item() <= 2e-5
