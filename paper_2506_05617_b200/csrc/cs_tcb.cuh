@@ -155,9 +155,11 @@ __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__
 // bits; the tensor core would truncate it to 11 -- a bias that accumulates
 // over super-rounds -- so it is rounded to tf32 here instead)
 __device__ __forceinline__ float rna_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    // = cvt.rna.tf32.f32 (round to nearest, ties away from zero) for finite x, in two integer
+    // instructions: ptxas expands the cvt into ~5 with an inf/nan pass-through, and the Gram staging
+    // (16 of them per thread and stage) is instruction-issue bound.  Non-finite input is caught by the
+    // exact fp32 column norms (rot_params), not here.
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ float lo_tf32(float x) { return rna_tf32(x - trunc_tf32(x)); }
 __device__ __forceinline__ float4 lo4(float4 x) {
