@@ -318,27 +318,44 @@ __device__ void expm_minus_identity(float2 *Em, float2 *Tm, float2 *Dm, float *r
 // block needs only S x [hi_b | lo_b]^T (M = 128, N = 64).  Also accumulates
 // this thread's share of the exact fp32 squared norm of real column
 // tid & 63 (the Gram diagonal).
-__device__ __forceinline__ void gram_stage2(const unsigned char *Pa, const unsigned char *Pb, int r0,
-                                            unsigned char *stg, float &nsq) {
+// The thread's addresses are stage-independent up to a constant: thread tid
+// handles real column j = tid & 63 and the row quads q0 = tid >> 6 and q0 + 8
+// of every stage, so the four swizzled load offsets and the store offset are
+// computed once per Gram (GramThr) instead of per stage -- the staging loop is
+// instruction-issue bound.
+struct GramThr {
+    const unsigned char *src;  // the column's panel + this thread's row-group offset
+    uint32_t ld[4];            // byte offsets of rows 4 q0 + d of a stage (row quad q0 + 8: + 4096)
+    uint32_t st;               // byte offset of the hi unit in the staging (lo: + 4096; row quad q0 + 8: + 16384)
+};
+__device__ __forceinline__ GramThr gram_thr(const unsigned char *Pa, const unsigned char *Pb) {
+    static_assert(NT == 512, "gram staging: 64 columns x 8 row quads per pass");
+    const int j = threadIdx.x & 63, q0 = threadIdx.x >> 6, k = j & 31;
+    GramThr g;
+    g.src = j < 32 ? Pa : Pb;
 #pragma unroll
-    for (int i = 0; i < 1024 / NT; ++i) {
-        const int u = threadIdx.x + i * NT, j = u & 63, rq = u >> 6;
-        const unsigned char *P = j < 32 ? Pa : Pb;
-        const int k = j & 31;
+    for (int d = 0; d < 4; ++d) g.ld[d] = so(4 * q0 + d, k);
+    const int hrow = j + (j & 32);  // hi_a 0..31, hi_b 64..95; lo 32 rows further
+    g.st = sw_chunk(hrow, q0, 16384);
+    return g;
+}
+__device__ __forceinline__ void gram_stage2(const GramThr &g, int st, unsigned char *stg, float &nsq) {
+    const unsigned char *src = g.src + st * 8192;  // 64 rows = 8 row groups of 1 KB
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
         float4 h;
-        h.x = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 0, k));
-        h.y = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 1, k));
-        h.z = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 2, k));
-        h.w = *reinterpret_cast<const float *>(P + so(r0 + 4 * rq + 3, k));
+        h.x = *reinterpret_cast<const float *>(src + i * 4096 + g.ld[0]);
+        h.y = *reinterpret_cast<const float *>(src + i * 4096 + g.ld[1]);
+        h.z = *reinterpret_cast<const float *>(src + i * 4096 + g.ld[2]);
+        h.w = *reinterpret_cast<const float *>(src + i * 4096 + g.ld[3]);
         nsq = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, nsq))));
         // round-to-nearest split (hi symmetric around x): the dropped lo*lo
         // term is then unbiased
         const float4 hr = make_float4(rna_tf32(h.x), rna_tf32(h.y), rna_tf32(h.z), rna_tf32(h.w));
         const float4 lr = make_float4(rna_tf32(h.x - hr.x), rna_tf32(h.y - hr.y), rna_tf32(h.z - hr.z),
                                       rna_tf32(h.w - hr.w));
-        const int hrow = j + (j & 32);  // hi_a 0..31, hi_b 64..95; lo 32 rows further
-        *reinterpret_cast<float4 *>(stg + sw_chunk(hrow, rq, 16384)) = hr;
-        *reinterpret_cast<float4 *>(stg + sw_chunk(hrow + 32, rq, 16384)) = lr;
+        *reinterpret_cast<float4 *>(stg + i * 16384 + g.st) = hr;
+        *reinterpret_cast<float4 *>(stg + i * 16384 + g.st + 4096) = lr;
     }
 }
 
@@ -562,12 +579,13 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 // accumulating its K-steps of every stage in accumulator w, so GW
                 // MMA streams run side by side.
                 float nsq = 0.f;
+                const GramThr gthr = gram_thr(Pa, Pb);
 #pragma unroll 1
                 for (int st = 0; st < K::STAGES; ++st) {
                     const int slot = st & 1;
                     if (st >= 2) gram_wait(slot);
                     if (wait_x) mbar_wait(&bar[6 + st], phx);  // the incoming panel's rows of this stage
-                    gram_stage2(Pa, Pb, 64 * st, RG + slot * 32768, nsq);
+                    gram_stage2(gthr, st, RG + slot * 32768, nsq);
                     fence_proxy_async_smem();
                     __syncthreads();
                     if (warp < GW) {
