@@ -130,7 +130,7 @@ struct Cfg {
     static constexpr uint32_t SIG_OFF = 3 * SLOT;
     static constexpr uint32_t PERM_OFF = SIG_OFF + NC * 4;
     static constexpr uint32_t FLAG_OFF = PERM_OFF + 2 * NC * 4;
-    static constexpr uint32_t RED_OFF = FLAG_OFF + 16 * 4;
+    static constexpr uint32_t RED_OFF = FLAG_OFF + 32 * 4;  // flags[16..31]: per-step cross-test stamps
     static constexpr uint32_t BAR_OFF = (RED_OFF + 64 * 4 + 15) & ~15u;
     static constexpr uint32_t TM_OFF = BAR_OFF + NBAR * 8;
     static constexpr uint32_t SMEM = TM_OFF + 16;
@@ -140,6 +140,7 @@ struct Cfg {
     static_assert(2 * NC >= 512, "the Gram norm partials reuse the permutation scratch");
     static_assert(C >= 2 && C <= MAXC, "tcb group size");
     static_assert(NBOX >= STEPS, "mailbox reuse must cross a sweep-verdict barrier");
+    static_assert(STEPS <= 16, "per-step stamps: 16 shared-memory words (flags[16..31])");
     static_assert(SMEM <= 227 * 1024, "tcb shared memory");
 };
 
@@ -435,7 +436,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         if (f >= a.count) break;
         const long long mid = a.index ? a.index[f] : f;
         ++mseq;
-        int sl[3] = {0, 1, 2};  // slots of panel a, panel b, scratch
+        // slots of panel a, panel b, scratch; stamps per role.  Scalars with selects, not arrays indexed by the
+        // outgoing role: dynamically indexed arrays live in local memory (LDL / STL stalls at every super-round)
+        int sl0 = 0, sl1 = 1, sl2 = 2;
         int ia = sc.ida[0][rank], ib = sc.idb[0][rank];
 #ifdef CS_TCB_CLOCKS
         bool tcb_on = true;
@@ -456,12 +459,12 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     const int r = e / (W / 2), j2 = e % (W / 2), j = (half == 0 ? ia : ib) * W + 2 * j2;
                     const float4 v = r < MR ? __ldg(reinterpret_cast<const float4 *>(X0 + (size_t)r * NC + j))
                                             : __ldg(reinterpret_cast<const float4 *>(V0 + (size_t)(r - MR) * NC + j));
-                    *reinterpret_cast<float4 *>(sm + sl[half] * SLOT + so4(r, j2)) = v;
+                    *reinterpret_cast<float4 *>(sm + half * SLOT + so4(r, j2)) = v;
                 }
             } else
             for (int half = 0; half < 2; ++half) {
                 const int c0 = (half == 0 ? ia : ib) * W;
-                unsigned char *P = sm + sl[half] * SLOT;
+                unsigned char *P = sm + half * SLOT;
                 for (int idx = tid; idx < K::ROWS * W; idx += NT) {
                     const int r = idx / W, jj = idx % W, j = c0 + jj;
                     float2 v;
@@ -491,9 +494,11 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         // modification and last within-panel test (they travel with the panel
         // through the exchange), per step this CTA's last cross test (CTA c meets
         // the same panel pair at step t in every sweep).
-        unsigned sr = 0, mod_r[2] = {0u, 0u}, wt_r[2] = {0u, 0u}, ctest[K::STEPS];
-#pragma unroll
-        for (int q = 0; q < K::STEPS; ++q) ctest[q] = 0u;
+        unsigned sr = 0, mod0 = 0u, mod1 = 0u, wt0 = 0u, wt1 = 0u;
+        // (CTA-uniform; in shared memory: every thread writes the same value, barriers separate it from the reads)
+        volatile unsigned *const ctest = reinterpret_cast<volatile unsigned *>(flags) + 16;
+        if (tid < K::STEPS) ctest[tid] = 0u;
+        __syncthreads();
         int src_pending = 0;
         auto finish_v = [&]() {  // the incoming V rows have landed
             if (wait_v) {
@@ -543,9 +548,9 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 const long long tcb_t0 = tcb_t;
                 if (tid == 0 && tcb_on) atomicAdd(&g_tcb_cycles[9], 1ull);
 #endif
-                unsigned char *const Pa = sm + sl[0] * SLOT;
-                unsigned char *const Pb = sm + sl[1] * SLOT;
-                unsigned char *const RG = sm + sl[2] * SLOT;
+                unsigned char *const Pa = sm + sl0 * SLOT;
+                unsigned char *const Pb = sm + sl1 * SLOT;
+                unsigned char *const RG = sm + sl2 * SLOT;
                 float2 *Dm = reinterpret_cast<float2 *>(RG + SC_D);
                 float2 *Gm = reinterpret_cast<float2 *>(RG + SC_G);
                 unsigned char *Bop = RG + SC_BOP;
@@ -556,8 +561,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 unsigned char *const outbox = box(rank, epoch + 1);
 
                 if (sr < 0xffffu) ++sr;  // stamps travel in 16 bits; saturated stamps never compare greater: no skips
-                const unsigned mod_max = mod_r[0] > mod_r[1] ? mod_r[0] : mod_r[1];
-                const bool skip = ctest[t] > mod_max && (!full || (wt_r[0] > mod_r[0] && wt_r[1] > mod_r[1]));
+                const unsigned mod_max = mod0 > mod1 ? mod0 : mod1;
+                const bool skip = ctest[t] > mod_max && (!full || (wt0 > mod0 && wt1 > mod1));
                 int any_rot = 0, any_big = 0, nact = 0;
                 bool act_mine = false, mma_upd = false;  // this thread's pair rotates; the tensor-core update ran
                 Prm<float> *prm = reinterpret_cast<Prm<float> *>(RG + SC_PRM);
@@ -722,8 +727,8 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     if (all >> 24) bad = true;
                 }
                 ctest[t] = sr;
-                if (full) wt_r[0] = wt_r[1] = sr;
-                if (any_rot && !bad) mod_r[0] = mod_r[1] = sr;
+                if (full) wt0 = wt1 = sr;
+                if (any_rot && !bad) mod0 = mod1 = sr;
                 }  // !skip
                 TCB_MARK(2);
                 if (vpend) {  // the previous sweep's verdict, before this sweep changes anything
@@ -1001,7 +1006,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                 if (xchg) {
                     const int src = fwd ? sc.src[t][rank] : sc.dst[t2][rank];
                     if (!mma_upd) {
-                        const float4 *sp = reinterpret_cast<const float4 *>(sm + sl[o] * SLOT);
+                        const float4 *sp = reinterpret_cast<const float4 *>(sm + (o ? sl1 : sl0) * SLOT);
                         float4 *dp = reinterpret_cast<float4 *>(outbox);
 #pragma unroll 4
                         for (int u = tid; u < (int)(SLOT / 16); u += NT) __stcg(dp + u, sp[u]);
@@ -1025,13 +1030,13 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                         // waits for the sender.
                         fence_proxy_async_global();
                         st_rel64(myctl + CT_META + 8 * (epoch % 16),
-                                 (unsigned long long)epoch | ((unsigned long long)(mod_r[o] & 0xffffu) << 32) |
-                                     ((unsigned long long)(wt_r[o] & 0xffffu) << 48));
+                                 (unsigned long long)epoch | ((unsigned long long)((o ? mod1 : mod0) & 0xffffu) << 32) |
+                                     ((unsigned long long)((o ? wt1 : wt0) & 0xffffu) << 48));
                     }
                     if (tid == 0) {
                         TCB_XCH(24);
                         const unsigned char *in = box(src, epoch);
-                        const uint32_t is = smem_u32(sm + sl[2] * SLOT);
+                        const uint32_t is = smem_u32(sm + sl2 * SLOT);
 #ifdef CS_TCB_CLOCKS
                         if ((int)((unsigned)ld_acq64(ctl(src) + CT_META + 8 * (epoch % 16)) - epoch) < 0)
                             if (tcb_on) atomicAdd(&g_tcb_cycles[28], 1ull);
@@ -1056,14 +1061,15 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     wait_x = true;
                     wait_v = VEC;
                     src_pending = src;
-                    const int ns = sl[2];
-                    sl[2] = sl[o];
-                    sl[o] = ns;
+                    const int ns = sl2;
+                    sl2 = o ? sl1 : sl0;
+                    if (o) sl1 = ns;
+                    else sl0 = ns;
                     ia = sc.ida[t2][rank];
                     ib = sc.idb[t2][rank];
                     __syncthreads();
-                    mod_r[o] = (unsigned)flags[4];  // the incoming panel's stamps
-                    wt_r[o] = (unsigned)flags[5];
+                    if (o) { mod1 = (unsigned)flags[4]; wt1 = (unsigned)flags[5]; }  // the incoming panel's stamps
+                    else { mod0 = (unsigned)flags[4]; wt0 = (unsigned)flags[5]; }
                 } else {
                     __syncthreads();
                 }
@@ -1099,7 +1105,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         float *gs = gsig + (mseq & 1) * NC;
         for (int c = warp; c < N2; c += NT / 32) {
             const int half = c / W, jj = c % W;
-            const unsigned char *P = sm + sl[half] * SLOT;
+            const unsigned char *P = sm + (half == 0 ? sl0 : sl1) * SLOT;
             float acc = 0.f;
             for (int r = lane; r < MR; r += 32) {
                 const float2 v = *reinterpret_cast<const float2 *>(P + so(r, 2 * jj));
@@ -1147,7 +1153,7 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
         __syncthreads();
         for (int half = 0; half < 2; ++half) {
             const int c0 = (half == 0 ? ia : ib) * W;
-            const unsigned char *P = sm + sl[half] * SLOT;
+            const unsigned char *P = sm + (half == 0 ? sl0 : sl1) * SLOT;
             if (a.Uw) {
                 for (int idx = tid; idx < MR * W; idx += NT) {
                     const int r = idx / W, jj = idx % W, j = c0 + jj;
