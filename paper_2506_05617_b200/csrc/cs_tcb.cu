@@ -708,7 +708,10 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
                     // "large": |gamma| / sqrt(alpha beta) > K3_TAU selects the exp combination
                     if (act > 0) act = (gv.x * gv.x + gv.y * gv.y > K3_TAU * K3_TAU * al * be) ? 2 : 1;
                     Prm<float> pm;
-                    pm.cm1 = R.cm1; pm.wr = R.wr; pm.wi = R.wi; pm.act = act;
+                    // a pair below the threshold is stored as the identity rotation, so the product form
+                    // below needs no per-round selects (x + 0 = x exactly)
+                    const bool on = act > 0;
+                    pm.cm1 = on ? R.cm1 : 0.f; pm.wr = on ? R.wr : 0.f; pm.wi = on ? R.wi : 0.f; pm.act = act;
                     prm[tid] = pm;
                 }
                 {
@@ -804,19 +807,15 @@ __global__ void __launch_bounds__(NT, 1) jacobi_tcb_kernel(const JacArgs<float> 
 #pragma unroll 4
                             for (int r = 0; r < W; ++r) {
                                 const Prm<float> pm = prm[r * W + k];
-                                // branch-free (the lanes of a half-warp differ in act): rotate
-                                // a copy and select it where the pair is active (a warp-uniform
-                                // skip of rounds without an active pair measured slower)
+                                // branch-free (the lanes of a half-warp differ in act): inactive
+                                // pairs are identity rotations (a warp-uniform skip of rounds
+                                // without an active pair measured slower)
                                 const int qq = W + ((k + r) & (W - 1));
                                 Rot<float> R;
                                 R.cm1 = pm.cm1; R.wr = pm.wr; R.wi = pm.wi;
-                                float2 xr = x, yr = y;
-                                rot_apply<float>(xr, yr, R);
-                                if (i2 == k) { xr.x += R.cm1; yr.x += R.wr; yr.y += R.wi; }
-                                if (i2 == qq) { xr.x -= R.wr; xr.y += R.wi; yr.x += R.cm1; }
-                                const bool on = pm.act > 0;
-                                x = on ? xr : x;
-                                y = on ? yr : y;
+                                rot_apply<float>(x, y, R);
+                                if (i2 == k) { x.x += R.cm1; y.x += R.wr; y.y += R.wi; }
+                                if (i2 == qq) { x.x -= R.wr; x.y += R.wi; y.x += R.cm1; }
                                 y.x = __shfl_sync(0xffffffffu, y.x, (k + 1) & (W - 1), W);
                                 y.y = __shfl_sync(0xffffffffu, y.y, (k + 1) & (W - 1), W);
                             }
